@@ -1,0 +1,144 @@
+/*
+ * misa_b200 — C ABI of the B200-native (sm_100a) MISA / DSA indexer.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * (passed as void*), is stream-ordered (no host synchronisation inside), keeps
+ * no device allocations across calls, and returns 0 on success or a negative
+ * error code; misa_last_error() holds a thread-local message.  The caller owns
+ * all memory (inputs, outputs, workspace).  Nothing here falls back to the CPU.
+ *
+ * Layouts (row-major, contiguous unless an ld is given):
+ *   keys      bf16 [n_keys][D]            D = head_dim padded to 64 or 128 (zero pad is exact)
+ *   queries   bf16 [n_rows][Hp][D]        Hp = n_heads padded to a power of two (>= 8)
+ *   weights   f32  [n_rows][Hp]           padded heads carry weight 0
+ *   prefix_len i32 [n_rows]               n_t: row t scores keys [0, n_t)
+ *   heads     i32 [n_rows][hq]            routed heads, ascending, -1 padded
+ *   topk      i32 [n_rows][topk_ld]       selected key indices, ascending, -1 padded
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/misa):
+ *   misa_pool_keys        pooling.py:57-84   build_block_summary (+ per-token in-block prefix sums)
+ *   misa_pool_append      pooling.py:87-115  incremental_append (decode)
+ *   misa_route_scores     routing.py:38-64   route_head_importance, block_attention GEMM part
+ *   misa_route_select     routing.py:38-75   route_head_importance epilogue + route_topk_heads
+ *   misa_score_materialize dsa.py:37-61, routing.py:78-99  gated_relu_scores / dsa_score / misa_score
+ *   misa_score_filter     dsa.py:37-76 fused with the candidate pass of topk_tokens
+ *   misa_select_threshold (no reference counterpart: sampled threshold for the fused top-k)
+ *   misa_select_topk      dsa.py:64-76       topk_tokens over the filtered candidates
+ *   misa_select_dense     dsa.py:64-92       topk_tokens / topk_within over a dense score row
+ *   misa_refine_scores    dsa.py:95-115      dsa_rescore (MISA-dagger fine stage), routing.py:144-174
+ *   misa_merge_topk       (no reference counterpart: key-sharded multi-GPU merge)
+ */
+#ifndef MISA_B200_H_
+#define MISA_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MISA_OK 0
+#define MISA_EINVAL (-1)       /* invalid argument / shape (the reference raises ValueError) */
+#define MISA_ECUDA (-2)        /* CUDA runtime / driver error */
+#define MISA_EUNSUPPORTED (-3) /* shape outside the compiled kernel set */
+
+/* router score kinds (config.py:14-17) */
+#define MISA_ROUTER_BLOCK_ATTENTION 0
+#define MISA_ROUTER_GATE_ONLY 1
+#define MISA_ROUTER_QUERY_NORM 2
+
+/* select flags (bit set per row in flags[]) */
+#define MISA_FLAG_OVERFLOW 1  /* more candidates than capacity: row must be re-selected densely */
+#define MISA_FLAG_UNDERFLOW 2 /* fewer candidates than min(k, n): threshold too high */
+
+int misa_abi_version(void);
+const char* misa_last_error(void);
+int misa_sm_count(void);
+
+/* K1: in-block inclusive prefix sums of the keys (f32 [n_keys][D]), full-block means
+ * (f32 [n_keys / B][D]) and their exact hi/mid/lo bf16 split (bf16 [3][planes_rows][D],
+ * rows >= n_keys / B zero-filled).  Any of the outputs may be NULL. */
+int misa_pool_keys(const void* keys, int64_t n_keys, int head_dim, int block_size, float* prefix_sums,
+                   float* pooled, void* pooled_planes, int64_t planes_rows, void* stream);
+
+/* Decode: append one key row.  prefix_sums row n_keys_before is written from row
+ * n_keys_before-1 (or started fresh at a block boundary); when the append closes a
+ * block its mean and planes row are written. */
+int misa_pool_append(const void* keys, int64_t n_keys_before, int head_dim, int block_size, float* prefix_sums,
+                     float* pooled, void* pooled_planes, int64_t planes_rows, void* stream);
+
+/* K2a: router partial sums.  partial[c][t][j] = sum over full blocks b in chunk c
+ * (128 blocks per chunk, b < n_t / B) of ReLU(q_tj . pooled_b), computed on tcgen05 with
+ * the pooled keys split into three bf16 planes (f32-grade); chunk 0 also adds
+ * ReLU(q_tj . partial-block mean) when n_t % B != 0.  Work list: item i covers the 128
+ * flattened (t, j) rows of tile it_tile[i] against block chunk it_chunk[i] with
+ * it_ncols[i] (multiple of 16, <= 128; 0 = partial-block term only) pooled columns;
+ * items are grouped by chunk.  Rows whose chunk c has no item are not written. */
+int misa_route_scores(const void* queries, int64_t n_rows, int n_heads_pad, int head_dim, const void* pooled_planes,
+                      int64_t planes_rows, const float* prefix_sums, const int32_t* prefix_len, int block_size,
+                      const int32_t* it_tile, const int32_t* it_chunk, const int32_t* it_ncols, int n_items,
+                      float* partial, void* stream);
+
+/* K2b: importance E_tj = |w_tj| * sum_c partial / ceil(n_t/B) (block_attention), w_tj
+ * (gate_only) or ||q_tj|| (query_norm); top-h heads (ties -> smaller head) ascending into
+ * heads[t][0..h), -1 padded to heads_ld.  importance may be NULL. */
+int misa_route_select(const float* partial, int n_chunks, const float* weights, const void* queries,
+                      const int32_t* prefix_len, int64_t n_rows, int n_heads, int n_heads_pad, int head_dim,
+                      int block_size, int h, int kind, int32_t* heads, int heads_ld, float* importance,
+                      void* stream);
+
+/* K3/K6 scoring on tcgen05.  Row t uses heads_per_query query vectors: heads[t][j]
+ * (MISA, -1 = empty slot) or head j < n_heads (DSA, heads == NULL).  Key s of row t is
+ * key row s*key_stride and valid for s < ceil(n_t / key_stride).  Work is given as
+ * groups of 256/heads_per_query consecutive rows (items[i] = group id, item_tiles[i]
+ * = number of 128-key tiles), scheduled longest first.
+ * materialize: out[t*out_ld + s] = score for valid s. */
+int misa_score_materialize(const void* keys, int64_t n_keys, int64_t key_stride, int head_dim,
+                           const void* queries, const float* weights, int n_heads, int n_heads_pad,
+                           const int32_t* heads, int heads_per_query, const int32_t* prefix_len, int64_t n_rows,
+                           const int32_t* items, const int32_t* item_tiles, int n_items, float* out,
+                           int64_t out_ld, void* stream);
+
+/* filter: append (score, s) with score >= tau[t] to cand[(t*4 + w)*cap + i] (w = TMEM lane
+ * quadrant of the key within its tile); cand_count[t*4 + w] = total seen (may exceed cap). */
+int misa_score_filter(const void* keys, int64_t n_keys, int head_dim, const void* queries, const float* weights,
+                      int n_heads, int n_heads_pad, const int32_t* heads, int heads_per_query,
+                      const int32_t* prefix_len, int64_t n_rows, const int32_t* items, const int32_t* item_tiles,
+                      int n_items, const float* tau, uint64_t* cand, int cap, int32_t* cand_count, void* stream);
+
+/* Per-row threshold: tau[t] = j-th largest sampled score, j = ceil(beta*k*m/n), m = ceil(n/stride);
+ * tau[t] = -inf when n <= append_all_len (every key is kept). */
+int misa_select_threshold(const float* sample_scores, int64_t ld, const int32_t* prefix_len, int64_t n_rows,
+                          int key_stride, int k, float beta, int64_t append_all_len, float* tau, void* stream);
+
+/* Exact top-k (score desc, index asc) from filtered candidates; output ascending indices.
+ * Rows with n_t <= k select [0, n_t).  topk_scores (optional) holds the scores aligned
+ * with topk.  flags[t] gets MISA_FLAG_* on overflow / underflow (row left -1). */
+int misa_select_topk(const uint64_t* cand, const int32_t* cand_count, int cap, const int32_t* prefix_len,
+                     int64_t n_rows, int k, int32_t* topk, int64_t topk_ld, float* topk_scores, int32_t* flags,
+                     void* stream);
+
+/* Exact top-k over dense rows: value scores[r*ld + i] for i < row_len[r] with index
+ * idx[r*idx_ld + i] (or i when idx == NULL); rows listed in rows[] (or all when NULL). */
+int misa_select_dense(const float* scores, int64_t ld, const int32_t* idx, int64_t idx_ld, const int32_t* row_len,
+                      const int32_t* rows, int64_t n_rows, int k, int32_t* topk, int64_t topk_ld,
+                      float* topk_scores, void* stream);
+
+/* MISA-dagger fine stage: out[t*out_ld + i] = sum_j w_tj ReLU(q_tj . key[cand[t][i]]) over all
+ * heads, for i < n_cand[t] (cand ascending, -1 padded), for the rows listed in rows[0..n_items)
+ * (longest first).  Gathered-key tcgen05 contraction (TMA tile::gather4). */
+int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const void* queries, const float* weights,
+                       int n_heads, int n_heads_pad, const int32_t* cand, int64_t cand_ld, const int32_t* n_cand,
+                       const int32_t* rows, int n_items, int64_t n_rows, float* out, int64_t out_ld, void* stream);
+
+/* Multi-GPU merge: n_parts local (score, index) top-k lists per row (parts[p][t][i], scores
+ * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc). */
+int misa_merge_topk(const float* part_scores, const int32_t* part_idx, int n_parts, int64_t part_stride,
+                    int64_t n_rows, int k_in, int k, int32_t* topk, int64_t topk_ld, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MISA_B200_H_ */

@@ -1,0 +1,270 @@
+// K5: MISA-dagger fine stage (dsa.py:95-115 dsa_rescore, routing.py:144-174).
+//
+// Row t re-scores its k' coarse candidates with ALL H heads:
+//   out[t][i] = sum_j w_{t,j} ReLU(q_{t,j} . k_{cand[t][i]})
+// The A operand is a gather of candidate key rows: TMA tile::gather4 moves four
+// arbitrary 128-byte rows per instruction straight into the 128-B-swizzled
+// K-major layout the UMMA descriptor expects (box {64, 1}).  B is the row's
+// Hp query heads (padded to N >= 16), resident in smem for the row's tiles.
+// The contraction is L2-bandwidth bound (the whole key set stays L2-resident:
+// 32 MiB at 128K), so the kernel keeps STAGES gathers in flight.
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace misa {
+
+struct RefineArgs {
+  const __nv_bfloat16* __restrict__ q;
+  const float* __restrict__ w;
+  const int32_t* __restrict__ cand;
+  int64_t cand_ld;
+  const int32_t* __restrict__ n_cand;
+  const int32_t* __restrict__ items;  // rows, longest first
+  int n_items;
+  int T, H, Hp;
+  float* out;
+  int64_t out_ld;
+};
+
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t col,
+                                            int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(ptx::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+template <int D, int N>
+struct RefineCfg {
+  static constexpr int STAGES = (D == 128) ? 5 : 8;
+  static constexpr int A_ATOM = 128 * 128;
+  static constexpr int A_BYTES = A_ATOM * (D / 64);
+  static constexpr int B_ATOM = N * 128;
+  static constexpr int B_BYTES = B_ATOM * (D / 64);
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = STAGES * A_BYTES;
+  static constexpr int OFF_W = OFF_B + ((B_BYTES + 1023) / 1024) * 1024;
+  static constexpr int OFF_BAR = OFF_W + N * 4;
+  static constexpr int NUM_BARS = 2 * STAGES + 5;
+  static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
+  static constexpr int TMEM_COLS = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : (2 * N <= 128) ? 128 : (2 * N <= 256) ? 256 : 512;
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
+};
+
+template <int D, int N>
+__global__ void __launch_bounds__(192, 1)
+    refine_kernel(const __grid_constant__ CUtensorMap tmap_k, const RefineArgs a) {
+  using C = RefineCfg<D, N>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + C::OFF_A;
+  uint8_t* sB = smem + C::OFF_B;
+  float* sW = reinterpret_cast<float*>(smem + C::OFF_W);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* full_a = bars;
+  uint64_t* empty_a = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = gridDim.x, bid = blockIdx.x;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmap_k);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full_a[i], 1);
+      ptx::mbar_init(&empty_a[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 128);
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto item_at = [&](int it) { return (it & 1) ? (it + 1) * P - 1 - bid : it * P + bid; };
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int it = 0;; ++it) {
+        const int idx = item_at(it);
+        if (idx >= a.n_items) break;
+        const int t = a.items[idx];
+        const int nc = a.n_cand[t];
+        const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
+        const int nt = (nc + 127) / 128;
+        for (int j = 0; j < nt; ++j) {
+          ptx::mbar_wait(&empty_a[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
+          for (int g = 0; g < 32; ++g) {
+            int r[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = j * 128 + 4 * g + e;
+              const int ki = i < nc ? cr[i] : 0;
+              r[e] = ki < 0 ? 0 : ki;
+            }
+#pragma unroll
+            for (int at = 0; at < D / 64; ++at)
+              tma_gather4(sA + s * C::A_BYTES + at * C::A_ATOM + g * 512, &tmap_k, &full_a[s], at * 64, r[0], r[1],
+                          r[2], r[3]);
+          }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (ptx::elect_one()) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      const uint32_t b_base = ptx::smem_u32(sB);
+      for (int it = 0;; ++it) {
+        const int idx = item_at(it);
+        if (idx >= a.n_items) break;
+        const int t = a.items[idx];
+        const int nt = (a.n_cand[t] + 127) / 128;
+        ptx::mbar_wait(bfull, it & 1);
+        ptx::tc_fence_after();
+        for (int j = 0; j < nt; ++j) {
+          ptx::mbar_wait(&tempty[acc], aph ^ 1);
+          ptx::mbar_wait(&full_a[s], ph);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
+          const uint32_t d_tmem = tmem_base + acc * N;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = (kk & 3) * 32;
+            const uint64_t ad = ptx::sw128_kmajor_desc(a_base + (kk >> 2) * C::A_ATOM + koff);
+            const uint64_t bd = ptx::sw128_kmajor_desc(b_base + (kk >> 2) * C::B_ATOM + koff);
+            ptx::mma_bf16(d_tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty_a[s]);
+          ptx::mma_commit(&tfull[acc]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+      }
+    }
+  } else {
+    const int et = threadIdx.x - 64;
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int it = 0;; ++it) {
+      const int idx = item_at(it);
+      if (idx >= a.n_items) break;
+      const int t = a.items[idx];
+      const int nc = a.n_cand[t];
+      const int nt = (nc + 127) / 128;
+      constexpr int CH = D / 8;
+      for (int c = et; c < N * CH; c += 128) {
+        const int r = c / CH, ch = c - r * CH;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < a.H) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)t * a.Hp + r) * D + ch * 8);
+        *reinterpret_cast<uint4*>(sB + ptx::sw128_offset(r, ch * 8, C::B_ATOM)) = v;
+      }
+      for (int r = et; r < N; r += 128) sW[r] = r < a.H ? a.w[(int64_t)t * a.Hp + r] : 0.f;
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (et == 0) ptx::mbar_arrive(bfull);
+      for (int j = 0; j < nt; ++j) {
+        ptx::mbar_wait(&tfull[acc], aph);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * N;
+        float sc = 0.f;
+#pragma unroll
+        for (int c = 0; c < N; c += 16) {
+          uint32_t r[16];
+          ptx::tmem_ld_x16(taddr + c, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) sc = fmaf(sW[c + jj], fmaxf(__uint_as_float(r[jj]), 0.f), sc);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+        const int i = j * 128 + quad * 32 + lane;
+        if (i < nc) a.out[(int64_t)t * a.out_ld + i] = sc;
+      }
+      ptx::named_bar_sync(1, 128);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int D, int N>
+static int launch_refine_t(const CUtensorMap& map, const RefineArgs& a, cudaStream_t st) {
+  using C = RefineCfg<D, N>;
+  auto kern = refine_kernel<D, N>;
+  MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+  const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
+  if (grid <= 0) return MISA_OK;
+  kern<<<grid, 192, C::SMEM_BYTES, st>>>(map, a);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}
+
+}  // namespace misa
+
+using namespace misa;
+
+extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                                  const float* weights, int n_heads, int n_heads_pad, const int32_t* cand,
+                                  int64_t cand_ld, const int32_t* n_cand, const int32_t* rows, int n_items,
+                                  int64_t n_rows, float* out, int64_t out_ld, void* stream) {
+  MISA_REQUIRE(keys && queries && weights && cand && n_cand && out && (rows || n_items == 0), "null pointer");
+  MISA_REQUIRE(head_dim == 64 || head_dim == 128, "head_dim must be padded to 64 or 128");
+  MISA_REQUIRE(n_heads >= 1 && n_heads <= n_heads_pad && n_heads_pad <= 128, "bad head counts");
+  MISA_REQUIRE(n_rows >= 1 && n_keys >= 1, "empty input");
+  if (n_items == 0) return MISA_OK;
+  CUtensorMap map;
+  int rc = make_tmap_bf16_gather(&map, keys, head_dim, n_keys);
+  if (rc) return rc;
+  RefineArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.w = weights;
+  a.cand = cand;
+  a.cand_ld = cand_ld;
+  a.n_cand = n_cand;
+  a.items = rows;
+  a.n_items = n_items;
+  a.T = (int)n_rows;
+  a.H = n_heads;
+  a.Hp = n_heads_pad;
+  a.out = out;
+  a.out_ld = out_ld;
+  cudaStream_t st = as_stream(stream);
+  const int N = n_heads_pad < 16 ? 16 : n_heads_pad;
+#define MISA_REFINE_CASE(DD, NN) \
+  if (head_dim == DD && N == NN) return launch_refine_t<DD, NN>(map, a, st);
+  MISA_REFINE_CASE(128, 16)
+  MISA_REFINE_CASE(128, 32)
+  MISA_REFINE_CASE(128, 64)
+  MISA_REFINE_CASE(128, 128)
+  MISA_REFINE_CASE(64, 16)
+  MISA_REFINE_CASE(64, 32)
+  MISA_REFINE_CASE(64, 64)
+  MISA_REFINE_CASE(64, 128)
+#undef MISA_REFINE_CASE
+  set_error("unsupported refine shape head_dim=%d heads=%d", head_dim, N);
+  return MISA_EUNSUPPORTED;
+}

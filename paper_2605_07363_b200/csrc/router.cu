@@ -1,0 +1,375 @@
+// K2: MISA head router (routing.py:38-75).
+//
+//   E_{t,j} = (1/M_t) * sum_{b < M_t} | w_{t,j} * ReLU(q_{t,j} . kbar_b) |,   M_t = ceil(n_t / B)
+//   heads_t = top-h of E_t (ties -> smaller head), ascending
+//
+// K2a (misa_route_scores) is a tcgen05 GEMM with the flattened (row, head) query
+// matrix on the UMMA M axis (128 (t,j) pairs per tile, TMA-loaded once — the Q
+// read is the HBM bound of the router) and up to 128 pooled full blocks on N.
+// The pooled means are f32; to keep the router at f32-grade precision they are
+// split into three bf16 planes (hi + mid + lo == the f32 value exactly) and the
+// K loop runs over the three planes into one accumulator, so
+// q . kbar = q . hi + q . mid + q . lo with exact bf16 products and f32 sums.
+// The epilogue thread owning (t, j) sums ReLU over the row's valid full blocks
+// and, in chunk 0, adds the row's partial last block from the in-block prefix
+// sums (mean over its real length, pooling.py:75-79).
+//
+// K2b (misa_route_select) applies |w| / M_t (or the gate_only / query_norm
+// importances), then one warp per row picks the top-h heads with warp argmax
+// rounds.
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace misa {
+
+struct RouteArgs {
+  const __nv_bfloat16* __restrict__ q;
+  const float* __restrict__ prefix;
+  const int32_t* __restrict__ prefix_len;
+  const int32_t* __restrict__ it_tile;
+  const int32_t* __restrict__ it_chunk;
+  const int32_t* __restrict__ it_ncols;
+  int n_items;
+  int T, Hp, hp_log2, B;
+  int64_t planes_rows;
+  float* partial;  // [n_chunks][T][Hp]
+};
+
+template <int D>
+struct RouteCfg {
+  static constexpr int STAGES = 4;
+  static constexpr int A_ATOM = 128 * 128;
+  static constexpr int A_BYTES = A_ATOM * (D / 64);
+  static constexpr int B_ATOM = 128 * 128;      // 128 pooled rows x 64 dims
+  static constexpr int B_PLANE = B_ATOM * (D / 64);
+  static constexpr int B_BYTES = 3 * B_PLANE;
+  static constexpr int NUM_THREADS = 192;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = STAGES * A_BYTES;
+  static constexpr int OFF_BAR = OFF_B + B_BYTES;
+  static constexpr int NUM_BARS = 2 * STAGES + 6;
+  static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
+};
+
+__device__ __forceinline__ int route_item(int it, int P, int b) { return (it & 1) ? (it + 1) * P - 1 - b : it * P + b; }
+
+template <int D>
+__global__ void __launch_bounds__(192, 1)
+    route_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_p,
+                 const RouteArgs a) {
+  using C = RouteCfg<D>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + C::OFF_A;
+  uint8_t* sB = smem + C::OFF_B;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* full_a = bars;
+  uint64_t* empty_a = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint64_t* bempty = bfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = gridDim.x, bid = blockIdx.x;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmap_q);
+    ptx::tma_prefetch_desc(&tmap_p);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full_a[i], 1);
+      ptx::mbar_init(&empty_a[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 128);
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::mbar_init(bempty, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 256);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      int s = 0, cur_chunk = -1, nb = 0;
+      uint32_t ph = 0;
+      for (int it = 0;; ++it) {
+        const int idx = route_item(it, P, bid);
+        if (idx >= a.n_items) break;
+        const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
+        if (ncols == 0) continue;
+        if (chunk != cur_chunk) {
+          if (nb > 0) ptx::mbar_wait(bempty, (nb - 1) & 1);
+          ptx::mbar_arrive_expect_tx(bfull, C::B_BYTES);
+          for (int p = 0; p < 3; ++p)
+            for (int at = 0; at < D / 64; ++at)
+              ptx::tma_load_2d(sB + p * C::B_PLANE + at * C::B_ATOM, &tmap_p, bfull, at * 64,
+                               (int)(p * a.planes_rows + chunk * 128));
+          cur_chunk = chunk;
+          ++nb;
+        }
+        ptx::mbar_wait(&empty_a[s], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
+        for (int at = 0; at < D / 64; ++at)
+          ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_q, &full_a[s], at * 64, a.it_tile[idx] * 128);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (ptx::elect_one()) {
+      int s = 0, acc = 0, cur_chunk = -1, nb = 0;
+      uint32_t ph = 0, aph = 0;
+      const uint32_t b_base = ptx::smem_u32(sB);
+      for (int it = 0;; ++it) {
+        const int idx = route_item(it, P, bid);
+        if (idx >= a.n_items) break;
+        const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
+        if (ncols == 0) continue;
+        if (chunk != cur_chunk) {
+          if (nb > 0) ptx::mma_commit(bempty);  // all MMAs on the previous chunk's planes
+          ptx::mbar_wait(bfull, nb & 1);
+          ptx::tc_fence_after();
+          cur_chunk = chunk;
+          ++nb;
+        }
+        ptx::mbar_wait(&tempty[acc], aph ^ 1);
+        ptx::mbar_wait(&full_a[s], ph);
+        ptx::tc_fence_after();
+        const uint32_t idesc = ptx::idesc_bf16_f32(128, ncols);
+        const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
+        const uint32_t d_tmem = tmem_base + acc * 128;
+        for (int p = 0; p < 3; ++p) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = (kk & 3) * 32;
+            const uint64_t ad = ptx::sw128_kmajor_desc(a_base + (kk >> 2) * C::A_ATOM + koff);
+            const uint64_t bd = ptx::sw128_kmajor_desc(b_base + p * C::B_PLANE + (kk >> 2) * C::B_ATOM + koff);
+            ptx::mma_bf16(d_tmem, ad, bd, idesc, (p | kk) ? 1u : 0u);
+          }
+        }
+        ptx::mma_commit(&empty_a[s]);
+        ptx::mma_commit(&tfull[acc]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int it = 0;; ++it) {
+      const int idx = route_item(it, P, bid);
+      if (idx >= a.n_items) break;
+      const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
+      const int64_t grow = (int64_t)a.it_tile[idx] * 128 + quad * 32 + lane;
+      const int t = (int)(grow >> a.hp_log2);
+      const int j = (int)(grow & (a.Hp - 1));
+      const int n = t < a.T ? a.prefix_len[t] : 0;
+      const int nf = n / a.B;
+      float sum = 0.f;
+      if (ncols > 0) {
+        ptx::mbar_wait(&tfull[acc], aph);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * 128;
+        const int lim = nf - chunk * 128;  // valid columns for this row
+        for (int c = 0; c < ncols; c += 32) {  // ncols is uniform per item
+          uint32_t r[32];
+          ptx::tmem_ld_x32(taddr + c, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c + i < lim) sum += fmaxf(__uint_as_float(r[i]), 0.f);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+      if (t < a.T) {
+        const int rem = n - nf * a.B;
+        if (chunk == 0 && rem > 0) {
+          // partial last block: mean over keys [nf*B, n) = P[n-1] / rem
+          const uint4* qv = reinterpret_cast<const uint4*>(a.q + grow * D);
+          const float4* pv = reinterpret_cast<const float4*>(a.prefix + (int64_t)(n - 1) * D);
+          float dot = 0.f;
+#pragma unroll 4
+          for (int c = 0; c < D / 8; ++c) {
+            const uint4 u = qv[c];
+            const float4 p0 = pv[2 * c], p1 = pv[2 * c + 1];
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+            float2 f;
+            f = __bfloat1622float2(h[0]); dot = fmaf(f.x, p0.x, dot); dot = fmaf(f.y, p0.y, dot);
+            f = __bfloat1622float2(h[1]); dot = fmaf(f.x, p0.z, dot); dot = fmaf(f.y, p0.w, dot);
+            f = __bfloat1622float2(h[2]); dot = fmaf(f.x, p1.x, dot); dot = fmaf(f.y, p1.y, dot);
+            f = __bfloat1622float2(h[3]); dot = fmaf(f.x, p1.z, dot); dot = fmaf(f.y, p1.w, dot);
+          }
+          sum += fmaxf(dot / (float)rem, 0.f);
+        }
+        a.partial[((int64_t)chunk * a.T + t) * a.Hp + j] = sum;
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 256);
+  }
+}
+
+// One warp per row: importance + top-h (value desc, head asc) -> ascending heads.
+__global__ void route_select_kernel(const float* __restrict__ partial, int n_chunks, const float* __restrict__ w,
+                                    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ prefix_len,
+                                    int T, int H, int Hp, int D, int B, int h, int kind, int32_t* __restrict__ heads,
+                                    int heads_ld, float* __restrict__ importance) {
+  const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp_g >= T) return;
+  const int t = warp_g;
+  const int n = prefix_len[t];
+  const int M = (n + B - 1) / B;
+  const int nf = n / B;
+  const int nch = nf > 0 ? (nf + 127) / 128 : 1;
+  float v[4];
+  bool taken[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int j = lane + 32 * r;
+    taken[r] = false;
+    v[r] = -INFINITY;
+    if (j < H) {
+      const float wj = w[(int64_t)t * Hp + j];
+      float e;
+      if (kind == MISA_ROUTER_GATE_ONLY) {
+        e = wj;
+      } else if (kind == MISA_ROUTER_QUERY_NORM) {
+        const __nv_bfloat16* qr = q + ((int64_t)t * Hp + j) * D;
+        float ss = 0.f;
+        for (int c = 0; c < D; ++c) {
+          const float x = __bfloat162float(qr[c]);
+          ss = fmaf(x, x, ss);
+        }
+        e = sqrtf(ss);
+      } else {
+        float s = 0.f;
+        for (int c = 0; c < nch && c < n_chunks; ++c) s += partial[((int64_t)c * T + t) * Hp + j];
+        e = fabsf(wj) * s / (float)M;
+      }
+      v[r] = e;
+      if (importance) importance[(int64_t)t * Hp + j] = e;
+    }
+  }
+  const int hh = h < H ? h : H;
+  for (int round = 0; round < hh; ++round) {
+    float best = -INFINITY;
+    int bj = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int j = lane + 32 * r;
+      if (j < H && !taken[r] && (v[r] > best || (v[r] == best && j < bj) || bj == 0x7fffffff)) {
+        best = v[r];
+        bj = j;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+      if (oj != 0x7fffffff && (bj == 0x7fffffff || ob > best || (ob == best && oj < bj))) {
+        best = ob;
+        bj = oj;
+      }
+    }
+    if ((bj & 31) == lane) taken[bj >> 5] = true;
+  }
+  int base = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, taken[r]);
+    if (taken[r]) heads[(int64_t)t * heads_ld + base + __popc(bal & ptx::lanemask_lt())] = lane + 32 * r;
+    base += __popc(bal);
+  }
+  for (int i = base + lane; i < heads_ld; i += 32) heads[(int64_t)t * heads_ld + i] = -1;
+}
+
+}  // namespace misa
+
+using namespace misa;
+
+// Work list: items (tile, chunk, ncols) precomputed on the host, chunk-major.
+extern "C" int misa_route_scores(const void* queries, int64_t n_rows, int n_heads_pad, int head_dim,
+                                 const void* pooled_planes, int64_t planes_rows, const float* prefix_sums,
+                                 const int32_t* prefix_len, int block_size, const int32_t* it_tile,
+                                 const int32_t* it_chunk, const int32_t* it_ncols, int n_items, float* partial,
+                                 void* stream) {
+  MISA_REQUIRE(queries && pooled_planes && prefix_sums && prefix_len && partial, "null pointer");
+  MISA_REQUIRE(head_dim == 64 || head_dim == 128, "head_dim must be padded to 64 or 128");
+  MISA_REQUIRE(n_heads_pad >= 1 && n_heads_pad <= 128 && (n_heads_pad & (n_heads_pad - 1)) == 0,
+               "n_heads_pad must be a power of two <= 128");
+  MISA_REQUIRE(block_size >= 1 && n_rows >= 1, "bad sizes");
+  MISA_REQUIRE(n_items == 0 || (it_tile && it_chunk && it_ncols), "null work list");
+  if (n_items == 0) return MISA_OK;
+  CUtensorMap mq, mp;
+  int rc = make_tmap_bf16_2d(&mq, queries, head_dim, (uint64_t)n_rows * n_heads_pad, head_dim, 128);
+  if (rc) return rc;
+  rc = make_tmap_bf16_2d(&mp, pooled_planes, head_dim, 3 * (uint64_t)planes_rows, head_dim, 128);
+  if (rc) return rc;
+  RouteArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.prefix = prefix_sums;
+  a.prefix_len = prefix_len;
+  a.it_tile = it_tile;
+  a.it_chunk = it_chunk;
+  a.it_ncols = it_ncols;
+  a.n_items = n_items;
+  a.T = (int)n_rows;
+  a.Hp = n_heads_pad;
+  a.hp_log2 = __builtin_ctz(n_heads_pad);
+  a.B = block_size;
+  a.planes_rows = planes_rows;
+  a.partial = partial;
+  cudaStream_t st = as_stream(stream);
+  const int grid = n_items < sm_count() ? n_items : sm_count();
+  if (head_dim == 128) {
+    MISA_CUDA_TRY(cudaFuncSetAttribute(route_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       RouteCfg<128>::SMEM_BYTES));
+    route_kernel<128><<<grid, 192, RouteCfg<128>::SMEM_BYTES, st>>>(mq, mp, a);
+  } else {
+    MISA_CUDA_TRY(cudaFuncSetAttribute(route_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       RouteCfg<64>::SMEM_BYTES));
+    route_kernel<64><<<grid, 192, RouteCfg<64>::SMEM_BYTES, st>>>(mq, mp, a);
+  }
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}
+
+extern "C" int misa_route_select(const float* partial, int n_chunks, const float* weights, const void* queries,
+                                 const int32_t* prefix_len, int64_t n_rows, int n_heads, int n_heads_pad,
+                                 int head_dim, int block_size, int h, int kind, int32_t* heads, int heads_ld,
+                                 float* importance, void* stream) {
+  MISA_REQUIRE(weights && prefix_len && heads, "null pointer");
+  MISA_REQUIRE(kind >= 0 && kind <= 2, "unknown router kind %d", kind);
+  MISA_REQUIRE(kind != MISA_ROUTER_BLOCK_ATTENTION || (partial && n_chunks >= 1), "null router partial sums");
+  MISA_REQUIRE(kind != MISA_ROUTER_QUERY_NORM || queries, "null queries");
+  MISA_REQUIRE(h >= 1, "h must be positive, got %d", h);
+  MISA_REQUIRE(n_heads >= 1 && n_heads <= n_heads_pad && n_heads_pad <= 128, "bad head counts");
+  MISA_REQUIRE(heads_ld >= (h < n_heads ? h : n_heads), "heads_ld too small");
+  MISA_REQUIRE(block_size >= 1 && n_rows >= 1, "bad sizes");
+  const int threads = 256;
+  const int64_t blocks = (n_rows * 32 + threads - 1) / threads;
+  route_select_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
+      partial, n_chunks, weights, static_cast<const __nv_bfloat16*>(queries), prefix_len, (int)n_rows, n_heads,
+      n_heads_pad, head_dim, block_size, h, kind, heads, heads_ld, importance);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}

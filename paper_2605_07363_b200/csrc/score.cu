@@ -1,0 +1,412 @@
+// K3 (MISA gathered-head scoring) and K6 (dense DSA scoring) on tcgen05.
+//
+//   I_{t,s} = sum_j w_{t,j} * ReLU(q_{t,j} . k_s)          (dsa.py:37-61, routing.py:78-99)
+//
+// One UMMA tile is D[128 keys x 256 cols] = K_tile[128 x D] * Bq[256 x D]^T where
+// the 256 columns are G = 256/HQ query rows x HQ head vectors (HQ = h routed heads
+// for MISA, all H heads for DSA).  Keys ride the M axis so that every TMEM lane
+// (one epilogue thread) owns one key and all heads of every query: the
+// ReLU / gate / head-sum epilogue is in-register with no shuffles.
+//
+// Warp roles (192 threads, 1 CTA per SM, persistent over work items):
+//   warp 0      TMA producer: 128-key tiles (box {64,128}, SWIZZLE_128B) into a
+//               STAGES-deep smem ring (mbarrier full/empty)
+//   warp 1      MMA issuer: one elected thread issues D/16 tcgen05.mma per tile
+//               into a double-buffered TMEM accumulator (2 x 256 columns)
+//   warps 2..5  epilogue: gather the item's query/head vectors into smem (the B
+//               operand, resident for the whole key scan), then per tile
+//               tcgen05.ld -> ReLU*w*sum -> either store the score row
+//               (MATERIALIZE) or append (score, key) >= tau to per-row candidate
+//               lists (FILTER: first pass of the fused top-k).
+//
+// A work item is a group of G consecutive query rows scanning key tiles
+// [0, ceil(max_t lim_t / 128)) — causal rows skip every tile past their prefix.
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace misa {
+
+struct ScoreArgs {
+  const __nv_bfloat16* __restrict__ q;  // [T][Hp][D]
+  const float* __restrict__ w;          // [T][Hp]
+  const int32_t* __restrict__ heads;    // [T][HQ] or nullptr (dense: head j)
+  const int32_t* __restrict__ prefix_len;
+  const int32_t* __restrict__ items;
+  const int32_t* __restrict__ item_tiles;
+  int n_items;
+  int T, H, Hp;
+  int key_stride;
+  float* out;
+  int64_t out_ld;
+  const float* __restrict__ tau;
+  uint64_t* cand;
+  int cap;
+  int32_t* cand_count;
+};
+
+template <int D, int HQ>
+struct ScoreCfg {
+  static constexpr int G = kTileCols / HQ;
+  static constexpr int STAGES = (D == 128) ? 4 : 6;
+  static constexpr int A_ATOM = kTileKeys * 128;   // bytes of one 64-wide K atom of a key tile
+  static constexpr int A_BYTES = A_ATOM * (D / 64);
+  static constexpr int B_ATOM = kTileCols * 128;
+  static constexpr int B_BYTES = B_ATOM * (D / 64);
+  static constexpr int NUM_THREADS = 64 + 32 * kQuadrants;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
+  static constexpr int OFF_W = OFF_B + B_BYTES;
+  static constexpr int OFF_LIM = OFF_W + kTileCols * 4;
+  static constexpr int OFF_TAU = OFF_LIM + 32 * 4;
+  static constexpr int OFF_BAR = OFF_TAU + 32 * 4;
+  static constexpr int NUM_BARS = 2 * STAGES + 5;
+  static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
+  static_assert(G >= 1 && G <= 32, "1..32 query rows per tile");
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
+};
+
+__device__ __forceinline__ int item_index(int it, int P, int b) {
+  // zigzag over CTAs: items are sorted longest first, so consecutive rounds
+  // alternate direction to balance the per-CTA total.
+  return (it & 1) ? (it + 1) * P - 1 - b : it * P + b;
+}
+
+template <int D, int HQ, bool FILTER>
+__global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
+    score_kernel(const __grid_constant__ CUtensorMap tmap_k, const ScoreArgs a) {
+  using C = ScoreCfg<D, HQ>;
+  constexpr int G = C::G;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + C::OFF_A;
+  uint8_t* sB = smem + C::OFF_B;
+  float* sW = reinterpret_cast<float*>(smem + C::OFF_W);
+  int* sLim = reinterpret_cast<int*>(smem + C::OFF_LIM);
+  float* sTau = reinterpret_cast<float*>(smem + C::OFF_TAU);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* full_a = bars;
+  uint64_t* empty_a = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int P = gridDim.x, bid = blockIdx.x;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmap_k);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full_a[i], 1);
+      ptx::mbar_init(&empty_a[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 32 * kQuadrants);
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (ptx::elect_one()) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int it = 0;; ++it) {
+        const int idx = item_index(it, P, bid);
+        if (idx >= a.n_items) break;
+        const int nt = a.item_tiles[idx];
+        for (int j = 0; j < nt; ++j) {
+          ptx::mbar_wait(&empty_a[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
+#pragma unroll
+          for (int at = 0; at < D / 64; ++at)
+            ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_k, &full_a[s], at * 64, j * kTileKeys);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
+    if (ptx::elect_one()) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kTileKeys, kTileCols);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      const uint32_t b_base = ptx::smem_u32(sB);
+      for (int it = 0;; ++it) {
+        const int idx = item_index(it, P, bid);
+        if (idx >= a.n_items) break;
+        const int nt = a.item_tiles[idx];
+        ptx::mbar_wait(bfull, it & 1);
+        ptx::tc_fence_after();
+        for (int j = 0; j < nt; ++j) {
+          ptx::mbar_wait(&tempty[acc], aph ^ 1);
+          ptx::mbar_wait(&full_a[s], ph);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
+          const uint32_t d_tmem = tmem_base + acc * kTileCols;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = (kk & 3) * 32;
+            const uint64_t ad = ptx::sw128_kmajor_desc(a_base + (kk >> 2) * C::A_ATOM + koff);
+            const uint64_t bd = ptx::sw128_kmajor_desc(b_base + (kk >> 2) * C::B_ATOM + koff);
+            ptx::mma_bf16(d_tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty_a[s]);
+          ptx::mma_commit(&tfull[acc]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------ epilogue
+    const int et = threadIdx.x - 64;  // 0..127
+    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
+    const uint32_t lane_mask_lt = ptx::lanemask_lt();
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int it = 0;; ++it) {
+      const int idx = item_index(it, P, bid);
+      if (idx >= a.n_items) break;
+      const int nt = a.item_tiles[idx];
+      const int row0 = a.items[idx] * G;
+
+      // B operand: row r = q*HQ + j <- Q[row0+q][head(q,j)][:], SW128 K-major layout.
+      constexpr int CH = D / 8;  // 16-byte chunks per row
+      for (int c = et; c < kTileCols * CH; c += 32 * kQuadrants) {
+        const int r = c / CH, ch = c - r * CH;
+        const int qi = r / HQ, j = r - qi * HQ;
+        const int row = row0 + qi;
+        int head = -1;
+        if (row < a.T) head = a.heads ? a.heads[(int64_t)row * HQ + j] : (j < a.H ? j : -1);
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (head >= 0) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)row * a.Hp + head) * D + ch * 8);
+        *reinterpret_cast<uint4*>(sB + ptx::sw128_offset(r, ch * 8, C::B_ATOM)) = v;
+      }
+      for (int r = et; r < kTileCols; r += 32 * kQuadrants) {
+        const int qi = r / HQ, j = r - qi * HQ;
+        const int row = row0 + qi;
+        float wv = 0.f;
+        if (row < a.T) {
+          const int head = a.heads ? a.heads[(int64_t)row * HQ + j] : (j < a.H ? j : -1);
+          if (head >= 0) wv = a.w[(int64_t)row * a.Hp + head];
+        }
+        sW[r] = wv;
+      }
+      if (et < G) {
+        const int row = row0 + et;
+        int lim = 0;
+        float tau = 0.f;
+        if (row < a.T) {
+          const int n = a.prefix_len[row];
+          lim = (n + a.key_stride - 1) / a.key_stride;
+          if (FILTER) tau = a.tau[row];
+        }
+        sLim[et] = lim;
+        sTau[et] = tau;
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 32 * kQuadrants);
+      if (et == 0) ptx::mbar_arrive(bfull);
+
+      int cnt = 0;  // FILTER: lane q counts candidates of query q seen by this warp
+      for (int jt = 0; jt < nt; ++jt) {
+        ptx::mbar_wait(&tfull[acc], aph);
+        ptx::tc_fence_after();
+        const int key = jt * kTileKeys + quad * 32 + lane;
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols;
+
+        auto emit = [&](int qi, float sc) {
+          const bool valid = key < sLim[qi];
+          const int row = row0 + qi;
+          if constexpr (FILTER) {
+            const bool pass = valid && (sc >= sTau[qi]);
+            const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+            if (bal) {
+              const int base = __shfl_sync(0xffffffffu, cnt, qi);
+              if (pass) {
+                const int pos = base + __popc(bal & lane_mask_lt);
+                if (pos < a.cap)
+                  a.cand[((int64_t)row * kQuadrants + quad) * a.cap + pos] =
+                      (static_cast<uint64_t>(static_cast<uint32_t>(key)) << 32) | __float_as_uint(sc);
+              }
+              if (lane == qi) cnt += __popc(bal);
+            }
+          } else {
+            if (valid) a.out[(int64_t)row * a.out_ld + key] = sc;
+          }
+        };
+
+        float part = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < kTileCols / 32; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld_x32(taddr + c * 32, r);
+          ptx::tmem_wait_ld();
+          if constexpr (HQ <= 32) {
+            constexpr int QPC = 32 / HQ;
+#pragma unroll
+            for (int qq = 0; qq < QPC; ++qq) {
+              const int qi = c * QPC + qq;
+              const float* wq = sW + qi * HQ;
+              float sc = 0.f;
+#pragma unroll
+              for (int jj = 0; jj < HQ; ++jj) sc = fmaf(wq[jj], fmaxf(__uint_as_float(r[qq * HQ + jj]), 0.f), sc);
+              emit(qi, sc);
+            }
+          } else {
+            const float* wq = sW + c * 32;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) part = fmaf(wq[jj], fmaxf(__uint_as_float(r[jj]), 0.f), part);
+            if (((c + 1) * 32) % HQ == 0) {
+              emit((c * 32) / HQ, part);
+              part = 0.f;
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+      if constexpr (FILTER) {
+        if (lane < G) {
+          const int row = row0 + lane;
+          if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = cnt;
+        }
+      }
+      ptx::named_bar_sync(1, 32 * kQuadrants);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+template <int D, int HQ, bool FILTER>
+static int launch_score_t(const CUtensorMap& map, const ScoreArgs& a, cudaStream_t st) {
+  using C = ScoreCfg<D, HQ>;
+  auto kern = score_kernel<D, HQ, FILTER>;
+  MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+  const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
+  if (grid <= 0) return MISA_OK;
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(map, a);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}
+
+template <bool FILTER>
+static int dispatch_score(int D, int HQ, const CUtensorMap& map, const ScoreArgs& a, cudaStream_t st) {
+#define MISA_SCORE_CASE(DD, HH) \
+  if (D == DD && HQ == HH) return launch_score_t<DD, HH, FILTER>(map, a, st);
+  MISA_SCORE_CASE(128, 8)
+  MISA_SCORE_CASE(128, 16)
+  MISA_SCORE_CASE(128, 32)
+  MISA_SCORE_CASE(128, 64)
+  MISA_SCORE_CASE(128, 128)
+  MISA_SCORE_CASE(64, 8)
+  MISA_SCORE_CASE(64, 16)
+  MISA_SCORE_CASE(64, 32)
+  MISA_SCORE_CASE(64, 64)
+  MISA_SCORE_CASE(64, 128)
+#undef MISA_SCORE_CASE
+  set_error("unsupported scoring shape: head_dim=%d heads_per_query=%d", D, HQ);
+  return MISA_EUNSUPPORTED;
+}
+
+static int check_common(int64_t n_keys, int D, int n_heads, int n_heads_pad, int hq, int64_t n_rows,
+                        const void* keys, const void* queries, const float* weights, const int32_t* prefix_len,
+                        const int32_t* items, const int32_t* item_tiles, int n_items) {
+  MISA_REQUIRE(keys && queries && weights && prefix_len, "null input pointer");
+  MISA_REQUIRE(n_items == 0 || (items && item_tiles), "null work list");
+  MISA_REQUIRE(n_keys >= 1 && n_rows >= 1, "empty keys or rows");
+  MISA_REQUIRE(D == 64 || D == 128, "head_dim must be padded to 64 or 128, got %d", D);
+  MISA_REQUIRE(n_heads >= 1 && n_heads <= n_heads_pad, "bad head counts %d/%d", n_heads, n_heads_pad);
+  MISA_REQUIRE(hq == 8 || hq == 16 || hq == 32 || hq == 64 || hq == 128, "heads_per_query %d", hq);
+  MISA_REQUIRE(n_rows < (int64_t(1) << 31) && n_keys < (int64_t(1) << 31), "too many rows/keys");
+  MISA_REQUIRE((reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(queries) & 15) == 0,
+               "keys/queries must be 16-byte aligned");
+  return MISA_OK;
+}
+
+}  // namespace misa
+
+using namespace misa;
+
+extern "C" int misa_score_materialize(const void* keys, int64_t n_keys, int64_t key_stride, int head_dim,
+                                      const void* queries, const float* weights, int n_heads, int n_heads_pad,
+                                      const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
+                                      int64_t n_rows, const int32_t* items, const int32_t* item_tiles, int n_items,
+                                      float* out, int64_t out_ld, void* stream) {
+  int rc = check_common(n_keys, head_dim, n_heads, n_heads_pad, heads_per_query, n_rows, keys, queries, weights,
+                        prefix_len, items, item_tiles, n_items);
+  if (rc) return rc;
+  MISA_REQUIRE(out && out_ld >= 1, "null output");
+  MISA_REQUIRE(key_stride >= 1, "key_stride must be >= 1");
+  MISA_REQUIRE(heads != nullptr || heads_per_query >= n_heads, "dense scoring needs heads_per_query >= n_heads");
+  const int64_t n_sample = (n_keys + key_stride - 1) / key_stride;
+  CUtensorMap map;
+  rc = make_tmap_bf16_2d(&map, keys, head_dim, n_sample, key_stride * head_dim, kTileKeys);
+  if (rc) return rc;
+  ScoreArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.w = weights;
+  a.heads = heads;
+  a.prefix_len = prefix_len;
+  a.items = items;
+  a.item_tiles = item_tiles;
+  a.n_items = n_items;
+  a.T = static_cast<int>(n_rows);
+  a.H = n_heads;
+  a.Hp = n_heads_pad;
+  a.key_stride = static_cast<int>(key_stride);
+  a.out = out;
+  a.out_ld = out_ld;
+  return dispatch_score<false>(head_dim, heads_per_query, map, a, as_stream(stream));
+}
+
+extern "C" int misa_score_filter(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                                 const float* weights, int n_heads, int n_heads_pad, const int32_t* heads,
+                                 int heads_per_query, const int32_t* prefix_len, int64_t n_rows,
+                                 const int32_t* items, const int32_t* item_tiles, int n_items, const float* tau,
+                                 uint64_t* cand, int cap, int32_t* cand_count, void* stream) {
+  int rc = check_common(n_keys, head_dim, n_heads, n_heads_pad, heads_per_query, n_rows, keys, queries, weights,
+                        prefix_len, items, item_tiles, n_items);
+  if (rc) return rc;
+  MISA_REQUIRE(tau && cand && cand_count && cap >= 1, "null filter buffers");
+  MISA_REQUIRE(heads != nullptr || heads_per_query >= n_heads, "dense scoring needs heads_per_query >= n_heads");
+  CUtensorMap map;
+  rc = make_tmap_bf16_2d(&map, keys, head_dim, n_keys, head_dim, kTileKeys);
+  if (rc) return rc;
+  ScoreArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.w = weights;
+  a.heads = heads;
+  a.prefix_len = prefix_len;
+  a.items = items;
+  a.item_tiles = item_tiles;
+  a.n_items = n_items;
+  a.T = static_cast<int>(n_rows);
+  a.H = n_heads;
+  a.Hp = n_heads_pad;
+  a.key_stride = 1;
+  a.tau = tau;
+  a.cand = cand;
+  a.cap = cap;
+  a.cand_count = cand_count;
+  return dispatch_score<true>(head_dim, heads_per_query, map, a, as_stream(stream));
+}
