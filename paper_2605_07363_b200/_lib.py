@@ -92,5 +92,13 @@ def check(rc: int, what: str = "") -> None:
     raise RuntimeError(f"misa_b200 error {rc}: {msg}")
 
 
+# entry points that launch device work (counted for the bench's gpu_launches claim)
+LAUNCHING = frozenset(n for n in SIGNATURES)
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     check(getattr(load(), name)(*args), name)
+    if name in LAUNCHING:
+        launch_count += 1

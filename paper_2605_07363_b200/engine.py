@@ -1,0 +1,383 @@
+"""Batched device engine: the performance path of the indexer.
+
+One call scores T query rows against a key cache on the GPU and returns the
+top-k token indices per row (ascending, -1 padded), the routed heads and,
+optionally, the router importances.  Row t is exactly the reference run on
+``IndexerWorkload(keys=K[:n_t], queries=Q[t], gate_weights=W[t])``
+(``workload.py:91-110``); the default ``prefix_len`` is causal prefill,
+n_t = L - T + t + 1 (``SPEC.md:79``: the query's own token is in the prefix).
+
+Pipeline per method (all kernels in ``csrc/``; every launch goes through the
+C ABI in ``include/misa_b200.h``):
+
+  dsa        score_materialize(sampled keys) -> select_threshold -> score_filter
+             (all H heads) -> select_topk                      (dsa.py:56-76,118-132)
+  misa       pool_keys -> route_scores -> route_select -> the same selector with
+             the h routed heads                                 (routing.py:102-141)
+  misa_hier  misa with k' -> refine_scores (all heads on the k' candidates)
+             -> select_dense within candidates                  (routing.py:144-174)
+
+The fused selector is exact: tau_t is the j-th largest score on a 1/stride key
+sample (j = ceil(beta*k*m/n)), every key with score >= tau_t is kept as a
+candidate, and when the candidate count is >= min(k, n_t) the exact top-k
+(score desc, index asc) provably lies among them.  Rows whose sample threshold
+was too high (underflow) or whose candidates overflow the buffer are re-done
+densely, so the result never depends on the estimate.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import BLOCK_ATTENTION, ROUTER_KIND_CODE, ROUTER_SCORE_KINDS
+from .validation import check_choice, check_positive_int
+
+METHODS = ("dsa", "misa", "misa_hier")
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _pow2(x: int) -> int:
+    return 1 << max(0, (int(x) - 1).bit_length())
+
+
+def head_dim_pad(d: int) -> int:
+    if d <= 64:
+        return 64
+    if d <= 128:
+        return 128
+    raise ValueError(f"head_dim {d} > 128 is not supported by the sm_100a kernels")
+
+
+def heads_pad(H: int) -> int:
+    if H > 128:
+        raise ValueError(f"n_heads {H} > 128 is not supported by the sm_100a kernels")
+    return max(8, _pow2(H))
+
+
+def heads_per_query(h: int) -> int:
+    return max(8, _pow2(h))
+
+
+@dataclass
+class IndexerOutput:
+    topk: torch.Tensor                  # (T, k) int32, ascending, -1 padded
+    heads: torch.Tensor | None = None   # (T, h) int32 ascending (misa / misa_hier)
+    importance: torch.Tensor | None = None  # (T, H) f32 router importance
+    candidates: torch.Tensor | None = None  # (T, k') int32 coarse candidates (misa_hier)
+    n_fallback_rows: int = 0
+
+
+@dataclass
+class PreparedInputs:
+    keys: torch.Tensor      # (L, D) bf16
+    queries: torch.Tensor   # (T, Hp, D) bf16
+    weights: torch.Tensor   # (T, Hp) f32
+    prefix: torch.Tensor    # (T,) int32 device
+    prefix_host: np.ndarray  # (T,) int64
+    L: int
+    T: int
+    H: int
+    Hp: int
+    d: int
+    D: int
+    causal_key: tuple | None
+
+
+def prepare_inputs(keys, queries, weights, prefix_len=None, device=None) -> PreparedInputs:
+    """Move/convert/pad inputs to the kernel layouts (no copy when already conforming)."""
+    dev = torch.device(device) if device is not None else (
+        keys.device if isinstance(keys, torch.Tensor) and keys.is_cuda else torch.device("cuda"))
+    K = torch.as_tensor(keys, device=dev)
+    Q = torch.as_tensor(queries, device=dev)
+    W = torch.as_tensor(weights, device=dev)
+    if K.ndim != 2 or Q.ndim != 3 or W.ndim != 2:
+        raise ValueError("keys must be (L, d), queries (T, H, d), weights (T, H)")
+    L, d = K.shape
+    T, H, dq = Q.shape
+    if dq != d:
+        raise ValueError(f"queries have dim {dq} but keys have dim {d}")
+    if tuple(W.shape) != (T, H):
+        raise ValueError(f"weights must be ({T}, {H}), got {tuple(W.shape)}")
+    if L < 1 or T < 1:
+        raise ValueError("need at least one key and one query row")
+    D, Hp = head_dim_pad(d), heads_pad(H)
+    K = K.to(torch.bfloat16)
+    if d != D:
+        K = torch.nn.functional.pad(K, (0, D - d))
+    K = K.contiguous()
+    Q = Q.to(torch.bfloat16)
+    if d != D or H != Hp:
+        Q = torch.nn.functional.pad(Q, (0, D - d, 0, Hp - H))
+    Q = Q.contiguous()
+    W = W.to(torch.float32)
+    if H != Hp:
+        W = torch.nn.functional.pad(W, (0, Hp - H))
+    W = W.contiguous()
+    causal_key = None
+    if prefix_len is None:
+        if T > L:
+            raise ValueError(f"causal prefill needs T <= L, got T={T}, L={L}")
+        host = np.arange(L - T + 1, L + 1, dtype=np.int64)
+        causal_key = (L, T)
+    else:
+        host = np.asarray(prefix_len.cpu() if isinstance(prefix_len, torch.Tensor) else prefix_len,
+                          dtype=np.int64).reshape(-1)
+        if host.shape[0] != T:
+            raise ValueError(f"prefix_len must have {T} entries")
+        if host.min() < 1 or host.max() > L:
+            raise ValueError("prefix lengths must lie in [1, L]")
+    prefix = torch.from_numpy(host.astype(np.int32)).to(dev)
+    return PreparedInputs(K, Q, W, prefix, host, L, T, H, Hp, d, D, causal_key)
+
+
+class IndexerEngine:
+    """Device indexer for one method/config; caches work lists and workspace per shape."""
+
+    def __init__(self, method: str = "misa", *, budget_k: int = 2048, active_heads_h: int = 8,
+                 block_size: int = 1024, candidate_kprime: int = 8192, router_score: str = BLOCK_ATTENTION,
+                 sample_stride: int = 32, beta: float | None = None, workspace_bytes: int = 16 << 30,
+                 check_overflow: bool = True):
+        check_choice(method, METHODS, "method")
+        self.method = method
+        self.k = check_positive_int(budget_k, "budget_k")
+        self.h = check_positive_int(active_heads_h, "active_heads_h")
+        self.B = check_positive_int(block_size, "block_size")
+        self.kprime = check_positive_int(candidate_kprime, "candidate_kprime")
+        if method == "misa_hier" and self.kprime < self.k:
+            raise ValueError(f"candidate_kprime ({self.kprime}) must be >= budget_k ({self.k})")
+        self.router_score = check_choice(router_score, ROUTER_SCORE_KINDS, "router_score")
+        self.stride = check_positive_int(sample_stride, "sample_stride")
+        self.beta = beta
+        self.workspace_bytes = workspace_bytes
+        self.check_overflow = check_overflow
+        self._ws: dict = {}
+        self._lists: dict = {}
+        self.last_fallback_rows = 0
+        self.stage_events: list | None = None  # set to [] to record (stage, cuda event) pairs
+        _lib.load()
+
+    def _mark(self, name: str) -> None:
+        if self.stage_events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.stage_events.append((name, ev))
+
+    # ----------------------------------------------------------- workspace
+    def _buf(self, name, shape, dtype, device):
+        n = int(np.prod(shape))
+        cur = self._ws.get(name)
+        if cur is None or cur.numel() < n or cur.dtype != dtype or cur.device != device:
+            cur = torch.empty(max(n, 1), dtype=dtype, device=device)
+            self._ws[name] = cur
+        return cur[:n].view(*shape)
+
+    def _cached(self, key, fn):
+        v = self._lists.get(key)
+        if v is None:
+            v = fn()
+            if len(self._lists) > 64:
+                self._lists.clear()
+            self._lists[key] = v
+        return v
+
+    @staticmethod
+    def _stream():
+        return torch.cuda.current_stream().cuda_stream
+
+    # ----------------------------------------------------------- work lists
+    @staticmethod
+    def group_items(lens: np.ndarray, G: int, stride: int, min_len: int) -> tuple[np.ndarray, np.ndarray]:
+        """Groups of G rows (group id, 128-key tiles) with some row longer than min_len, longest first."""
+        T = lens.shape[0]
+        ng = (T + G - 1) // G
+        pad = np.zeros(ng * G, dtype=np.int64)
+        pad[:T] = lens
+        mx = pad.reshape(ng, G).max(1)
+        keep = np.nonzero(mx > min_len)[0]
+        tiles = ((mx[keep] + stride - 1) // stride + 127) // 128
+        order = np.argsort(-tiles, kind="stable")
+        return keep[order].astype(np.int32), tiles[order].astype(np.int32)
+
+    def _route_items(self, lens: np.ndarray, Hp: int, n_chunks: int):
+        T = lens.shape[0]
+        rpt = 128 // Hp
+        ntiles = (T * Hp + 127) // 128
+        pad = np.zeros(ntiles * rpt, dtype=np.int64)
+        pad[:T] = lens // self.B
+        nf = pad.reshape(ntiles, rpt).max(1)
+        tl, ch, cols = [], [], []
+        for c in range(n_chunks):
+            cc = np.clip(nf - 128 * c, 0, 128)
+            cc = (cc + 15) // 16 * 16
+            sel = np.arange(ntiles) if c == 0 else np.nonzero(cc > 0)[0]
+            order = sel[np.argsort(-cc[sel], kind="stable")]
+            tl.append(order)
+            ch.append(np.full(order.shape[0], c))
+            cols.append(cc[order])
+        return tuple(np.concatenate(x).astype(np.int32) for x in (tl, ch, cols))
+
+    def _dev_list(self, key, fn, device):
+        def make():
+            arrs = fn()
+            return tuple(torch.from_numpy(np.ascontiguousarray(a)).to(device) for a in arrs)
+        return self._cached(key, make)
+
+    # ----------------------------------------------------------- stages
+    def pool(self, x: PreparedInputs):
+        """K1: in-block prefix sums + pooled planes."""
+        nf = x.L // self.B
+        n_chunks = max(1, (nf + 127) // 128)
+        rows = n_chunks * 128
+        P = self._buf("prefix", (x.L, x.D), torch.float32, x.keys.device)
+        planes = self._buf("planes", (3, rows, x.D), torch.bfloat16, x.keys.device)
+        self._mark("pool")
+        _lib.call("misa_pool_keys", _ptr(x.keys), x.L, x.D, self.B, _ptr(P), None, _ptr(planes), rows, self._stream())
+        return P, planes, n_chunks, rows
+
+    def route(self, x: PreparedInputs, need_importance: bool = False):
+        """K2: heads (T, hq) int32 ascending, -1 padded; importance (T, Hp) f32 or None."""
+        h = min(self.h, x.H)
+        hq = heads_per_query(h)
+        dev = x.keys.device
+        kind = ROUTER_KIND_CODE[self.router_score]
+        heads = self._buf("heads", (x.T, hq), torch.int32, dev)
+        imp = self._buf("importance", (x.T, x.Hp), torch.float32, dev) if need_importance else None
+        partial, n_chunks = None, 1
+        if self.router_score == BLOCK_ATTENTION:
+            P, planes, n_chunks, rows = self.pool(x)
+            key = ("route", x.causal_key or x.prefix_host.tobytes(), x.Hp, self.B, n_chunks)
+            it_tile, it_chunk, it_cols = self._dev_list(key, lambda: self._route_items(x.prefix_host, x.Hp, n_chunks),
+                                                        dev)
+            partial = self._buf("partial", (n_chunks, x.T, x.Hp), torch.float32, dev)
+            self._mark("route_scores")
+            _lib.call("misa_route_scores", _ptr(x.queries), x.T, x.Hp, x.D, _ptr(planes), rows, _ptr(P),
+                      _ptr(x.prefix), self.B, _ptr(it_tile), _ptr(it_chunk), _ptr(it_cols), it_tile.numel(),
+                      _ptr(partial), self._stream())
+        self._mark("route_select")
+        _lib.call("misa_route_select", _ptr(partial), n_chunks, _ptr(x.weights), _ptr(x.queries), _ptr(x.prefix),
+                  x.T, x.H, x.Hp, x.D, self.B, h, kind, _ptr(heads), hq, _ptr(imp), self._stream())
+        return heads, hq, imp
+
+    def select(self, x: PreparedInputs, heads: torch.Tensor | None, hq: int, k: int, out: torch.Tensor,
+               tag: str = "sel") -> int:
+        """Fused streaming top-k over the given head set (None = all heads). Returns #fallback rows."""
+        dev = x.keys.device
+        beta = self.beta if self.beta is not None else (2.0 if k < 4096 else 1.5)
+        cap = max(64, int(math.ceil(beta * k / 2)))        # per TMEM quadrant; total 4*cap
+        cap = (cap + 7) // 8 * 8
+        append_all = 4 * cap
+        G = 256 // hq
+        stream = self._stream()
+        ckey = x.causal_key or x.prefix_host.tobytes()
+        s_items, s_tiles = self._dev_list(("samp", ckey, G, self.stride, append_all),
+                                          lambda: self.group_items(x.prefix_host, G, self.stride, append_all), dev)
+        f_items, f_tiles = self._dev_list(("filt", ckey, G, k),
+                                          lambda: self.group_items(x.prefix_host, G, 1, k), dev)
+        Ls = (x.L + self.stride - 1) // self.stride
+        tau = self._buf(tag + "_tau", (x.T,), torch.float32, dev)
+        if s_items.numel():
+            samp = self._buf(tag + "_samp", (x.T, Ls), torch.float32, dev)
+            self._mark(tag + ":sample")
+            _lib.call("misa_score_materialize", _ptr(x.keys), x.L, self.stride, x.D, _ptr(x.queries), _ptr(x.weights),
+                      x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(s_items), _ptr(s_tiles), s_items.numel(),
+                      _ptr(samp), Ls, stream)
+        else:
+            samp = self._buf(tag + "_samp", (1, 1), torch.float32, dev)
+        self._mark(tag + ":threshold")
+        _lib.call("misa_select_threshold", _ptr(samp), Ls, _ptr(x.prefix), x.T, self.stride, k, float(beta),
+                  append_all, _ptr(tau), stream)
+        cand = self._buf(tag + "_cand", (x.T * 4 * cap,), torch.int64, dev)
+        cnt = self._buf(tag + "_cnt", (x.T * 4,), torch.int32, dev)
+        if f_items.numel():
+            self._mark(tag + ":filter")
+            _lib.call("misa_score_filter", _ptr(x.keys), x.L, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
+                      _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(f_items), _ptr(f_tiles), f_items.numel(), _ptr(tau),
+                      _ptr(cand), cap, _ptr(cnt), stream)
+        flags = self._buf(tag + "_flags", (x.T,), torch.int32, dev)
+        self._mark(tag + ":select")
+        _lib.call("misa_select_topk", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, _ptr(out), out.stride(0),
+                  None, _ptr(flags), stream)
+        self._mark(tag + ":end")
+        if not self.check_overflow:
+            return 0
+        bad = torch.nonzero(flags).flatten()
+        if bad.numel() == 0:
+            return 0
+        self._dense_rows(x, heads, hq, k, out, bad.cpu().numpy())
+        return int(bad.numel())
+
+    def _dense_rows(self, x: PreparedInputs, heads, hq, k, out, rows: np.ndarray):
+        """Exact fallback: materialize full score rows for the flagged rows' groups, dense select."""
+        dev = x.keys.device
+        G = 256 // hq
+        stream = self._stream()
+        scratch = self._buf("dense_scratch", (G, x.L), torch.float32, dev)
+        for g in np.unique(rows // G):
+            r0 = int(g) * G
+            nmax = int(x.prefix_host[r0:r0 + G].max())
+            items = torch.tensor([g], dtype=torch.int32, device=dev)
+            tiles = torch.tensor([(nmax + 127) // 128], dtype=torch.int32, device=dev)
+            base = scratch.data_ptr() - r0 * x.L * 4  # row t of the group lands in scratch[t - r0]
+            _lib.call("misa_score_materialize", _ptr(x.keys), x.L, 1, x.D, _ptr(x.queries), _ptr(x.weights), x.H,
+                      x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles), 1, base, x.L, stream)
+            sel = torch.from_numpy(rows[(rows // G) == g].astype(np.int32)).to(dev)
+            _lib.call("misa_select_dense", base, x.L, None, 0, _ptr(x.prefix), _ptr(sel), sel.numel(), k, _ptr(out),
+                      out.stride(0), None, stream)
+
+    def refine(self, x: PreparedInputs, cand: torch.Tensor, k: int, out: torch.Tensor):
+        """K5 + dense select within candidates (MISA-dagger fine stage)."""
+        dev = x.keys.device
+        kp = cand.shape[1]
+        ncand_host = np.minimum(x.prefix_host, kp)
+        ckey = x.causal_key or x.prefix_host.tobytes()
+        ncand, rows = self._dev_list(("refine", ckey, kp),
+                                     lambda: (ncand_host.astype(np.int32),
+                                              np.argsort(-ncand_host, kind="stable").astype(np.int32)), dev)
+        rs = self._buf("refine_scores", (x.T, kp), torch.float32, dev)
+        stream = self._stream()
+        self._mark("refine")
+        _lib.call("misa_refine_scores", _ptr(x.keys), x.L, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
+                  _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(rows), rows.numel(), x.T, _ptr(rs), kp, stream)
+        self._mark("refine_select")
+        _lib.call("misa_select_dense", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), None, x.T, k,
+                  _ptr(out), out.stride(0), None, stream)
+        self._mark("refine:end")
+
+    # ----------------------------------------------------------- entry
+    def run(self, keys, queries, weights, prefix_len=None, *, need_importance: bool = False,
+            out: torch.Tensor | None = None) -> IndexerOutput:
+        x = prepare_inputs(keys, queries, weights, prefix_len)
+        return self.run_prepared(x, need_importance=need_importance, out=out)
+
+    def run_prepared(self, x: PreparedInputs, *, need_importance: bool = False,
+                     out: torch.Tensor | None = None) -> IndexerOutput:
+        dev = x.keys.device
+        k = self.k
+        if out is None:
+            out = torch.empty(x.T, k, dtype=torch.int32, device=dev)
+        if self.method == "dsa":
+            nfb = self.select(x, None, x.Hp, k, out)
+            self.last_fallback_rows = nfb
+            return IndexerOutput(topk=out, n_fallback_rows=nfb)
+        heads, hq, imp = self.route(x, need_importance)
+        h = min(self.h, x.H)
+        if self.method == "misa":
+            nfb = self.select(x, heads, hq, k, out)
+            self.last_fallback_rows = nfb
+            return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H],
+                                 n_fallback_rows=nfb)
+        kp = max(self.kprime, k)
+        cand = self._buf("hier_cand", (x.T, kp), torch.int32, dev)
+        nfb = self.select(x, heads, hq, kp, cand, tag="coarse")
+        self.refine(x, cand, k, out)
+        self.last_fallback_rows = nfb
+        return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H],
+                             candidates=cand, n_fallback_rows=nfb)
