@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark: MISA indexer ms/layer at 128K causal prefill (H=64, h=8) vs the dense DSA kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--L 131072]
+
+One step = one indexer layer: all T = L query rows of a causal prefill scored
+against the L-key cache, top-k = 2048 per row (BASELINE.json configs[3] shape,
+the C4 workload of SURVEY.md §8).  Inputs are synthetic (torch randn keys and
+queries, softmax gates, seed 0) and device-resident for ``value``; ``e2e``
+repeats the step through the public estimator API with host->device copies of
+K/Q/W from pinned memory and a device->host read of the top-k each step.  The
+queries (2 GiB) exceed the 126 MB L2, so no explicit L2 flush is used.
+
+Under torchrun (N > 1) the key axis is sharded block-cyclically across ranks,
+each rank emits a local top-k with scores and an NCCL all-gather + merge kernel
+produces the global top-k (strong scaling: the layer is fixed); timing is the
+max over ranks.
+
+``--impl reference`` times the reference algorithm on the host CPU (the oracle
+port in ``oracle/``; the reference is Python and cannot be compiled) on the same
+config and metric: a bounded stratified sample of rows per step, extrapolated
+to one layer.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "indexer ms/layer at 128K (H^I=64,h=8) + speedup vs dense DSA; top-k recall"
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--L", type=int, default=131072)
+    p.add_argument("--H", type=int, default=64)
+    p.add_argument("--h", type=int, default=8)
+    p.add_argument("--d", type=int, default=128)
+    p.add_argument("--B", type=int, default=1024)
+    p.add_argument("--k", type=int, default=2048)
+    p.add_argument("--kprime", type=int, default=8192)
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--hier", action="store_true", help="also time MISA-dagger (k'=--kprime)")
+    return p.parse_args()
+
+
+def _workload_name(a):
+    return f"C4 causal prefill L=T={a.L} H={a.H} h={a.h} d={a.d} B={a.B} k={a.k}"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["hbm_gbs"], pk["bf16_tflops"], pk["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(a):
+    """--impl reference: the reference algorithm (oracle port) on host cores, same metric/config."""
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu_bench
+    from oracle import misa_oracle as O
+    gen = torch.Generator().manual_seed(0)
+    K = torch.randn(a.L, a.d, generator=gen).bfloat16().double().numpy()
+    cores = os.cpu_count() or 1
+    rows = cpu_bench.sample_rows(a.L, a.L, max(16, 2 * cores))
+    rng = np.random.default_rng(0)
+    Qr = O.bf16_round(rng.standard_normal((len(rows), a.H, a.d)))
+    Wr = O.softmax_rows(rng.standard_normal((len(rows), a.H)))
+    vals = []
+    info = None
+    for i in range(a.warmup + a.steps):
+        info = cpu_bench.time_layer("misa", K, Qr, Wr, rows, a.L, a.L, k=a.k, h=a.h, B=a.B, kp=a.kprime,
+                                    cores=cores)
+        if i >= a.warmup:
+            vals.append(info["ms_per_layer"])
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "ms/layer", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": v, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (fast32)", "data": "synthetic",
+            "config": {"workload": _workload_name(a), "L": a.L, "T": a.L, "H": a.H, "h": a.h, "d": a.d,
+                       "B": a.B, "k": a.k},
+            "cpu_baseline": {"value": v, "unit": "ms/layer", "cores": cores, "kind": "port",
+                             "sample": f"{info['rows']} stratified causal rows per step, per-row reference "
+                                       f"misa select (pool+route+score+top-k, fast32), extrapolated "
+                                       f"linearly in prefix length over all {a.L} rows / {cores} cores"},
+            "e2e": {"value": v, "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _time_steps(fn, steps, warmup, barrier):
+    import torch
+    for _ in range(warmup):
+        fn()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_07363_b200 import _lib, MISAIndexer, DSAIndexer, IndexerEngine, prepare_inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    L, T = a.L, a.L
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    K = torch.randn(L, a.d, device="cuda", generator=gen).bfloat16()
+    Q = torch.randn(T, a.H, a.d, device="cuda", generator=gen).bfloat16()
+    W = torch.softmax(torch.randn(T, a.H, device="cuda", generator=gen), -1).float()
+    hbm, tc_burst, tc_sust, peak_src = _peaks()
+
+    if world > 1:
+        from paper_2605_07363_b200.sharded import ShardedIndexer
+        eng_m = ShardedIndexer("misa", world=world, rank=rank, budget_k=a.k, active_heads_h=a.h, block_size=a.B)
+        eng_d = ShardedIndexer("dsa", world=world, rank=rank, budget_k=a.k, block_size=a.B)
+    else:
+        eng_m = IndexerEngine("misa", budget_k=a.k, active_heads_h=a.h, block_size=a.B)
+        eng_d = IndexerEngine("dsa", budget_k=a.k)
+    x = prepare_inputs(K, Q, W) if world == 1 else None
+
+    def step_m():
+        return eng_m.run_prepared(x) if world == 1 else eng_m.run(K, Q, W)
+
+    def step_d():
+        return eng_d.run_prepared(x) if world == 1 else eng_d.run(K, Q, W)
+
+    # --- MISA (the headline value), with clocks sampled during the timed region
+    launches0 = _lib.launch_count
+    with Clocks(local) as clk:
+        misa_ms = _time_steps(step_m, a.steps, a.warmup, barrier)
+    launches = (_lib.launch_count - launches0) // (a.steps + a.warmup) * a.steps
+    misa_ms = max_over_ranks(misa_ms)
+    clocks = clk.summary()
+    fallback = eng_m.last_fallback_rows if hasattr(eng_m, "last_fallback_rows") else 0
+
+    # --- per-stage device times of one MISA step (events on the launching stream)
+    stages = {}
+    if world == 1:
+        eng_m.stage_events = []
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        res_m = step_m()
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record()
+        torch.cuda.synchronize()
+        ev = eng_m.stage_events + [("end", t1)]
+        for (n0, e0), (_, e1) in zip(ev, ev[1:]):
+            stages[n0] = stages.get(n0, 0.0) + e0.elapsed_time(e1)
+        eng_m.stage_events = None
+    else:
+        res_m = step_m()
+
+    # --- dense DSA on the same inputs (the comparison kernel)
+    dsa_ms = max_over_ranks(_time_steps(step_d, a.steps, a.warmup, barrier))
+    dstages = {}
+    if world == 1:
+        eng_d.stage_events = []
+        res_d = step_d()
+        torch.cuda.synchronize()
+        ev = eng_d.stage_events
+        for (n0, e0), (_, e1) in zip(ev, ev[1:]):
+            dstages[n0] = dstages.get(n0, 0.0) + e0.elapsed_time(e1)
+        eng_d.stage_events = None
+    else:
+        res_d = step_d()
+
+    hier_ms = None
+    hstages = {}
+    if a.hier and world == 1:
+        eng_h = IndexerEngine("misa_hier", budget_k=a.k, active_heads_h=a.h, block_size=a.B,
+                              candidate_kprime=a.kprime)
+        hier_ms = _time_steps(lambda: eng_h.run_prepared(x), a.steps, a.warmup, barrier)
+        eng_h.stage_events = []
+        eng_h.run_prepared(x)
+        torch.cuda.synchronize()
+        ev = eng_h.stage_events
+        hstages = {}
+        for (n0, e0), (_, e1) in zip(ev, ev[1:]):
+            hstages[n0] = hstages.get(n0, 0.0) + e0.elapsed_time(e1)
+        eng_h.stage_events = None
+
+    # --- e2e through the public API: pinned host buffers, H2D each step, D2H of the top-k
+    e2e = None
+    if not a.no_e2e:
+        Kh, Qh, Wh = K.cpu().pin_memory(), Q.cpu().pin_memory(), W.cpu().pin_memory()
+        Kd, Qd, Wd = torch.empty_like(K), torch.empty_like(Q), torch.empty_like(W)
+        out_h = torch.empty(T, a.k, dtype=torch.int32).pin_memory()
+        est = MISAIndexer(budget_k=a.k, active_heads_h=a.h, block_size=a.B)
+        if world > 1:
+            est_engine = eng_m
+
+        def step_e2e():
+            Kd.copy_(Kh, non_blocking=True)
+            Qd.copy_(Qh, non_blocking=True)
+            Wd.copy_(Wh, non_blocking=True)
+            r = est.select_batch(Kd, Qd, Wd) if world == 1 else est_engine.run(Kd, Qd, Wd)
+            out_h.copy_(r.topk, non_blocking=True)
+
+        e2e_ms = max_over_ranks(_time_steps(step_e2e, a.steps, max(1, a.warmup), barrier))
+        h2d = K.numel() * 2 + Q.numel() * 2 + W.numel() * 4
+        e2e = {"value": e2e_ms, "unit": "ms/layer", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(T * a.k * 4)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # --- recall vs the CPU reference algorithm on sampled rows (oracle, fast32, same bf16 inputs)
+    from oracle import misa_oracle as O
+    rows = sorted(set([2048, 8192, T // 4, T // 2, 3 * T // 4, T - 1]))
+    Kn = K.double().cpu().numpy()
+    hit = tot = 0
+    iou = []
+    for t in rows:
+        n = t + 1
+        qs, ws = Q[t].double().cpu().numpy(), W[t].double().cpu().numpy()
+        ref = O.misa_select(Kn[:n], qs, ws, a.k, a.h, a.B, precision="fast32")["selection"]
+        got = res_m.topk[t].cpu().numpy()
+        got = set(got[got >= 0].tolist())
+        hit += len(got & set(ref.tolist()))
+        tot += len(ref)
+        gd = res_d.topk[t].cpu().numpy()
+        gd = set(gd[gd >= 0].tolist())
+        iou.append(len(got & gd) / len(got | gd))
+    recall = hit / tot
+
+    # --- roofline of the dominant kernel (MISA token scoring, tcgen05)
+    P = L * (L + 1) // 2                       # causal scored pairs per layer
+    flops_misa = 2.0 * a.h * a.d * P           # 2*h*d per score
+    filt_ms = stages.get("sel:filter")
+    traffic = None
+    prof = os.path.join(REPO, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("score_filter_misa", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = None
+    if filt_ms:
+        ach = flops_misa / (filt_ms * 1e-3) / 1e12
+        roof = {"kernel": "score_kernel<128,8,FILTER> (MISA routed-head scoring + fused top-k filter)",
+                "bound": "tensor", "achieved": round(ach, 1), "peak": tc_sust, "unit": "TFLOP/s",
+                "frac": round(ach / tc_sust, 4), "traffic": traffic,
+                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a multi-kernel step)",
+                "flops_per_launch": flops_misa, "launch_ms": round(filt_ms, 3)}
+    layer_frac = flops_misa / (misa_ms * 1e-3) / 1e12 / tc_sust
+
+    cpu = None
+    if not a.no_cpu:
+        from oracle import cpu_bench
+        cores = os.cpu_count() or 1
+        srows = cpu_bench.sample_rows(L, T, max(16, 2 * cores))
+        Qs = Q[torch.as_tensor(srows)].double().cpu().numpy()
+        Ws = W[torch.as_tensor(srows)].double().cpu().numpy()
+        info = cpu_bench.time_layer("misa", Kn, Qs, Ws, srows, L, T, k=a.k, h=a.h, B=a.B, kp=a.kprime, cores=cores)
+        cpu = {"value": round(info["ms_per_layer"], 1), "unit": "ms/layer", "cores": cores, "kind": "port",
+               "sample": f"{info['rows']} stratified causal rows of this workload, per-row reference misa select "
+                         f"(pool+route+score+top-k, fast32) in {cores} single-BLAS-thread processes "
+                         f"({info['cpu_s']:.1f} s CPU), extrapolated linearly in prefix length to all {T} rows"}
+
+    line = {
+        "metric": METRIC, "value": round(misa_ms, 3), "unit": "ms/layer", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(misa_ms, 3), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (torch randn keys/queries, softmax gates, seed 0)",
+        "config": {"workload": _workload_name(a), "L": L, "T": T, "H": a.H, "h": a.h, "d": a.d, "B": a.B,
+                   "k": a.k, "parallelism": f"key-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (queries 2 GiB); no explicit flush"},
+        "dsa_ms_per_layer": round(dsa_ms, 3), "speedup_vs_dsa": round(dsa_ms / misa_ms, 3),
+        "topk_recall_vs_cpu_reference": round(recall, 6), "recall_rows": rows,
+        "misa_iou_vs_dsa_random_data": round(float(np.mean(iou)), 4),
+        "scores_per_s": P / (misa_ms * 1e-3), "layer_tensor_frac": round(layer_frac, 4),
+        "misa_stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "dsa_stages_ms": {k: round(v, 4) for k, v in dstages.items()},
+        "fallback_rows": fallback,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
+    }
+    if hier_ms is not None:
+        line["misa_hier_ms_per_layer"] = round(hier_ms, 3)
+        line["misa_hier_stages_ms"] = {k: round(v, 4) for k, v in hstages.items()}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -130,6 +130,28 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// wait::ld that also "redefines" the destination registers of the outstanding
+// loads, so the compiler cannot hoist their uses above the wait.
+__device__ __forceinline__ void tmem_wait_ld_dep(uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+        "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+        "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+        "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld_dep16(uint32_t* r) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+        "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+      :
+      : "memory");
+}
+
 // 32 lanes x 32 consecutive 32-bit columns: thread i gets lane (base_lane + i), cols [c, c+32).
 __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -195,4 +217,22 @@ __device__ __forceinline__ float key_float(uint32_t k) {
   return __uint_as_float(u);
 }
 
+}  // namespace misa
+
+namespace misa {
+// Gated-ReLU head reduction shared by every scorer so that identical inputs give
+// bit-identical scores on every path (dense, routed, refine): heads are consumed
+// in groups of four into two packed-f32x2 accumulators,
+//   s0 += (w0, w1) * (relu x0, relu x1),  s1 += (w2, w3) * (relu x2, relu x3),
+// and a query's score is (s0.x + s0.y) + (s1.x + s1.y).
+__device__ __forceinline__ void gate_relu4(float2& s0, float2& s1, const float4 w, uint32_t x0, uint32_t x1,
+                                           uint32_t x2, uint32_t x3) {
+  s0 = __ffma2_rn(make_float2(w.x, w.y),
+                  make_float2(fmaxf(__uint_as_float(x0), 0.f), fmaxf(__uint_as_float(x1), 0.f)), s0);
+  s1 = __ffma2_rn(make_float2(w.z, w.w),
+                  make_float2(fmaxf(__uint_as_float(x2), 0.f), fmaxf(__uint_as_float(x3), 0.f)), s1);
+}
+__device__ __forceinline__ float gate_relu_finish(const float2 s0, const float2 s1) {
+  return (s0.x + s0.y) + (s1.x + s1.y);
+}
 }  // namespace misa

@@ -95,34 +95,40 @@ __global__ void __launch_bounds__(192, 1)
   auto item_at = [&](int it) { return (it & 1) ? (it + 1) * P - 1 - bid : it * P + bid; };
 
   if (warp == 0) {
-    if (ptx::elect_one()) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int it = 0;; ++it) {
-        const int idx = item_at(it);
-        if (idx >= a.n_items) break;
-        const int t = a.items[idx];
-        const int nc = a.n_cand[t];
-        const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
-        const int nt = (nc + 127) / 128;
-        for (int j = 0; j < nt; ++j) {
+    // Producer warp: lane l gathers candidate rows 4l..4l+3 of each 128-row tile
+    // (one coalesced index load per lane, one tile::gather4 per lane and K atom).
+    int s = 0;
+    uint32_t ph = 0;
+    for (int it = 0;; ++it) {
+      const int idx = item_at(it);
+      if (idx >= a.n_items) break;
+      const int t = a.items[idx];
+      const int nc = a.n_cand[t];
+      const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
+      const int nt = (nc + 127) / 128;
+      auto load_idx = [&](int j, int (&r)[4]) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = j * 128 + 4 * lane + e;
+          const int ki = i < nc ? cr[i] : 0;
+          r[e] = ki < 0 ? 0 : ki;
+        }
+      };
+      int rn[4];
+      if (nt > 0) load_idx(0, rn);
+      for (int j = 0; j < nt; ++j) {
+        int r[4] = {rn[0], rn[1], rn[2], rn[3]};
+        if (j + 1 < nt) load_idx(j + 1, rn);  // next tile's indices in flight while this one issues
+        if (lane == 0) {
           ptx::mbar_wait(&empty_a[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
-          for (int g = 0; g < 32; ++g) {
-            int r[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = j * 128 + 4 * g + e;
-              const int ki = i < nc ? cr[i] : 0;
-              r[e] = ki < 0 ? 0 : ki;
-            }
-#pragma unroll
-            for (int at = 0; at < D / 64; ++at)
-              tma_gather4(sA + s * C::A_BYTES + at * C::A_ATOM + g * 512, &tmap_k, &full_a[s], at * 64, r[0], r[1],
-                          r[2], r[3]);
-          }
-          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
+        __syncwarp();
+#pragma unroll
+        for (int at = 0; at < D / 64; ++at)
+          tma_gather4(sA + s * C::A_BYTES + at * C::A_ATOM + lane * 512, &tmap_k, &full_a[s], at * 64, r[0], r[1],
+                      r[2], r[3]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -184,15 +190,28 @@ __global__ void __launch_bounds__(192, 1)
         ptx::mbar_wait(&tfull[acc], aph);
         ptx::tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * N;
-        float sc = 0.f;
+        // same head order / accumulators as the scorer (ptx.cuh gate_relu4), so an
+        // all-head re-score reproduces the dense DSA score bit for bit
+        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+        const float4* w4 = reinterpret_cast<const float4*>(sW);
+        uint32_t ra[16], rb[16];
+        ptx::tmem_ld_x16(taddr, ra);
+        ptx::tmem_wait_ld_dep16(ra);
 #pragma unroll
-        for (int c = 0; c < N; c += 16) {
-          uint32_t r[16];
-          ptx::tmem_ld_x16(taddr + c, r);
-          ptx::tmem_wait_ld();
+        for (int c = 0; c < N; c += 32) {
+          if (c + 16 < N) ptx::tmem_ld_x16(taddr + c + 16, rb);
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) sc = fmaf(sW[c + jj], fmaxf(__uint_as_float(r[jj]), 0.f), sc);
+          for (int jj = 0; jj < 16; jj += 4) gate_relu4(s0, s1, w4[(c + jj) / 4], ra[jj], ra[jj + 1], ra[jj + 2], ra[jj + 3]);
+          if (c + 16 < N) {
+            ptx::tmem_wait_ld_dep16(rb);
+            if (c + 32 < N) ptx::tmem_ld_x16(taddr + c + 32, ra);
+#pragma unroll
+            for (int jj = 0; jj < 16; jj += 4)
+              gate_relu4(s0, s1, w4[(c + 16 + jj) / 4], rb[jj], rb[jj + 1], rb[jj + 2], rb[jj + 3]);
+            if (c + 32 < N) ptx::tmem_wait_ld_dep16(ra);
+          }
         }
+        const float sc = gate_relu_finish(s0, s1);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }

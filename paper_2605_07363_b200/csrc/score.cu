@@ -8,16 +8,19 @@
 // (one epilogue thread) owns one key and all heads of every query: the
 // ReLU / gate / head-sum epilogue is in-register with no shuffles.
 //
-// Warp roles (192 threads, 1 CTA per SM, persistent over work items):
+// Warp roles (64 + 32*EPI_WARPS threads, 1 CTA per SM, persistent over work items):
 //   warp 0      TMA producer: 128-key tiles (box {64,128}, SWIZZLE_128B) into a
 //               STAGES-deep smem ring (mbarrier full/empty)
 //   warp 1      MMA issuer: one elected thread issues D/16 tcgen05.mma per tile
 //               into a double-buffered TMEM accumulator (2 x 256 columns)
-//   warps 2..5  epilogue: gather the item's query/head vectors into smem (the B
-//               operand, resident for the whole key scan), then per tile
-//               tcgen05.ld -> ReLU*w*sum -> either store the score row
-//               (MATERIALIZE) or append (score, key) >= tau to per-row candidate
-//               lists (FILTER: first pass of the fused top-k).
+//   warps 2..   epilogue (16 warps, 8 when a query has 128 heads; warp w drains
+//               TMEM lane quadrant w%4 and one column split): gather
+//               the item's query/head vectors into smem (the B operand, resident
+//               for the whole key scan), then per tile a software-pipelined
+//               tcgen05.ld drain -> ReLU * w * sum (packed FFMA2) -> either store
+//               the score row (MATERIALIZE) or append (score, key) >= tau to the
+//               row's per-quadrant candidate list (FILTER: the fused top-k's
+//               candidate pass; lists stay in ascending key order).
 //
 // A work item is a group of G consecutive query rows scanning key tiles
 // [0, ceil(max_t lim_t / 128)) — causal rows skip every tile past their prefix.
@@ -25,6 +28,47 @@
 #include "ptx.cuh"
 
 namespace misa {
+
+// Reduce one 16-column TMEM chunk (warp-local chunk C of its COLS columns) into the
+// per-query scores sc[]: HQ columns per query row, gate weights from smem.
+template <int HQ, int QW, int C>
+__device__ __forceinline__ void reduce16(const uint32_t* r, const float* __restrict__ wcol, float (&sc)[QW],
+                                         float2& p0, float2& p1) {
+  const float4* w4 = reinterpret_cast<const float4*>(wcol + C * 16);
+  if constexpr (HQ <= 16) {
+    constexpr int QPC = 16 / HQ;
+#pragma unroll
+    for (int qq = 0; qq < QPC; ++qq) {
+      float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < HQ; jj += 4) {
+        const int b = qq * HQ + jj;
+        gate_relu4(s0, s1, w4[b / 4], r[b], r[b + 1], r[b + 2], r[b + 3]);
+      }
+      sc[C * QPC + qq] = gate_relu_finish(s0, s1);
+    }
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < 16; jj += 4) gate_relu4(p0, p1, w4[jj / 4], r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
+    if constexpr (((C + 1) * 16) % HQ == 0) {
+      sc[(C * 16) / HQ] = gate_relu_finish(p0, p1);
+      p0 = make_float2(0.f, 0.f);
+      p1 = make_float2(0.f, 0.f);
+    }
+  }
+}
+
+// Drain chunks [C, NCH) of a warp's COLS TMEM columns, x16 loads double-buffered.
+template <int HQ, int QW, int NCH, int C>
+__device__ __forceinline__ void drain(uint32_t taddr, const float* __restrict__ wcol, float (&sc)[QW], float2& p0,
+                                      float2& p1, uint32_t (&ra)[16], uint32_t (&rb)[16]) {
+  if constexpr (C < NCH) {
+    if constexpr (C + 1 < NCH) ptx::tmem_ld_x16(taddr + (C + 1) * 16, (C & 1) ? ra : rb);
+    reduce16<HQ, QW, C>((C & 1) ? rb : ra, wcol, sc, p0, p1);
+    if constexpr (C + 1 < NCH) ptx::tmem_wait_ld_dep16((C & 1) ? ra : rb);
+    drain<HQ, QW, NCH, C + 1>(taddr, wcol, sc, p0, p1, ra, rb);
+  }
+}
 
 struct ScoreArgs {
   const __nv_bfloat16* __restrict__ q;  // [T][Hp][D]
@@ -46,23 +90,31 @@ struct ScoreArgs {
 
 template <int D, int HQ>
 struct ScoreCfg {
-  static constexpr int G = kTileCols / HQ;
+  static constexpr int G = kTileCols / HQ;             // query rows per item
+  static constexpr int SPLIT = (HQ <= 64) ? 4 : 2;     // column splits per TMEM quadrant
+  static constexpr int EPI_WARPS = kQuadrants * SPLIT;  // 16 or 8
+  static constexpr int EPI_THREADS = 32 * EPI_WARPS;
+  static constexpr int COLS = kTileCols / SPLIT;       // TMEM columns per epilogue warp
+  static constexpr int QW = COLS >= HQ ? COLS / HQ : 1;  // query rows per epilogue warp
+  static constexpr int NCH = COLS / 16;
   static constexpr int STAGES = (D == 128) ? 4 : 6;
   static constexpr int A_ATOM = kTileKeys * 128;   // bytes of one 64-wide K atom of a key tile
   static constexpr int A_BYTES = A_ATOM * (D / 64);
   static constexpr int B_ATOM = kTileCols * 128;
   static constexpr int B_BYTES = B_ATOM * (D / 64);
-  static constexpr int NUM_THREADS = 64 + 32 * kQuadrants;
+  static constexpr int NUM_THREADS = 64 + EPI_THREADS;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
   static constexpr int OFF_W = OFF_B + B_BYTES;
   static constexpr int OFF_LIM = OFF_W + kTileCols * 4;
   static constexpr int OFF_TAU = OFF_LIM + 32 * 4;
-  static constexpr int OFF_BAR = OFF_TAU + 32 * 4;
+  static constexpr int OFF_STG = OFF_TAU + 32 * 4;  // FILTER append staging: [warp][QW][32] f32
+  static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * QW * 32 * 4;
   static constexpr int NUM_BARS = 2 * STAGES + 5;
   static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
-  static_assert(G >= 1 && G <= 32, "1..32 query rows per tile");
+  static_assert(G >= 2 && G <= 32, "2..32 query rows per tile");
+  static_assert(QW * SPLIT == G, "query rows split evenly over the column splits");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
 
@@ -76,8 +128,7 @@ template <int D, int HQ, bool FILTER>
 __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
     score_kernel(const __grid_constant__ CUtensorMap tmap_k, const ScoreArgs a) {
   using C = ScoreCfg<D, HQ>;
-  constexpr int G = C::G;
-  constexpr int STAGES = C::STAGES;
+  constexpr int G = C::G, STAGES = C::STAGES, QW = C::QW, EPI_THREADS = C::EPI_THREADS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem + C::OFF_A;
@@ -85,6 +136,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
   float* sW = reinterpret_cast<float*>(smem + C::OFF_W);
   int* sLim = reinterpret_cast<int*>(smem + C::OFF_LIM);
   float* sTau = reinterpret_cast<float*>(smem + C::OFF_TAU);
+  float* sStg = reinterpret_cast<float*>(smem + C::OFF_STG);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* full_a = bars;
   uint64_t* empty_a = bars + STAGES;
@@ -105,7 +157,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 32 * kQuadrants);
+      ptx::mbar_init(&tempty[i], EPI_THREADS);
     }
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
@@ -170,9 +222,13 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------ epilogue
-    const int et = threadIdx.x - 64;  // 0..127
-    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
-    const uint32_t lane_mask_lt = ptx::lanemask_lt();
+    // warp w reads TMEM lane quadrant (w % 4) and column split (w - 2) / 4:
+    // COLS columns = QW query rows of each 128 x 256 accumulator tile.
+    const int e = warp - 2;
+    const int et = threadIdx.x - 64;
+    const int quad = warp & 3;
+    const int split = e >> 2;
+    float* stg = sStg + e * (QW * 32);
     int acc = 0;
     uint32_t aph = 0;
     for (int it = 0;; ++it) {
@@ -183,7 +239,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
 
       // B operand: row r = q*HQ + j <- Q[row0+q][head(q,j)][:], SW128 K-major layout.
       constexpr int CH = D / 8;  // 16-byte chunks per row
-      for (int c = et; c < kTileCols * CH; c += 32 * kQuadrants) {
+      for (int c = et; c < kTileCols * CH; c += EPI_THREADS) {
         const int r = c / CH, ch = c - r * CH;
         const int qi = r / HQ, j = r - qi * HQ;
         const int row = row0 + qi;
@@ -193,7 +249,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         if (head >= 0) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)row * a.Hp + head) * D + ch * 8);
         *reinterpret_cast<uint4*>(sB + ptx::sw128_offset(r, ch * 8, C::B_ATOM)) = v;
       }
-      for (int r = et; r < kTileCols; r += 32 * kQuadrants) {
+      for (int r = et; r < kTileCols; r += EPI_THREADS) {
         const int qi = r / HQ, j = r - qi * HQ;
         const int row = row0 + qi;
         float wv = 0.f;
@@ -216,75 +272,79 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         sTau[et] = tau;
       }
       ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 32 * kQuadrants);
+      ptx::named_bar_sync(1, EPI_THREADS);
       if (et == 0) ptx::mbar_arrive(bfull);
 
-      int cnt = 0;  // FILTER: lane q counts candidates of query q seen by this warp
+      const int qbase = split * QW;  // first query row (within the item) of this warp
+      int lim_r[QW];
+      float tau_r[QW];
+#pragma unroll
+      for (int q = 0; q < QW; ++q) {
+        lim_r[q] = sLim[qbase + q];
+        tau_r[q] = sTau[qbase + q];
+      }
+      const float* wcol = sW + split * C::COLS;
+      int cnt = 0;  // FILTER: lane q counts candidates of query qbase+q seen by this warp
+      uint64_t* dst = nullptr;
+      if (FILTER && lane < QW) dst = a.cand + ((int64_t)(row0 + qbase + lane) * kQuadrants + quad) * a.cap;
       for (int jt = 0; jt < nt; ++jt) {
         ptx::mbar_wait(&tfull[acc], aph);
         ptx::tc_fence_after();
-        const int key = jt * kTileKeys + quad * 32 + lane;
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols;
-
-        auto emit = [&](int qi, float sc) {
-          const bool valid = key < sLim[qi];
-          const int row = row0 + qi;
-          if constexpr (FILTER) {
-            const bool pass = valid && (sc >= sTau[qi]);
-            const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-            if (bal) {
-              const int base = __shfl_sync(0xffffffffu, cnt, qi);
-              if (pass) {
-                const int pos = base + __popc(bal & lane_mask_lt);
-                if (pos < a.cap)
-                  a.cand[((int64_t)row * kQuadrants + quad) * a.cap + pos] =
-                      (static_cast<uint64_t>(static_cast<uint32_t>(key)) << 32) | __float_as_uint(sc);
-              }
-              if (lane == qi) cnt += __popc(bal);
-            }
-          } else {
-            if (valid) a.out[(int64_t)row * a.out_ld + key] = sc;
-          }
-        };
-
-        float part = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < kTileCols / 32; ++c) {
-          uint32_t r[32];
-          ptx::tmem_ld_x32(taddr + c * 32, r);
-          ptx::tmem_wait_ld();
-          if constexpr (HQ <= 32) {
-            constexpr int QPC = 32 / HQ;
-#pragma unroll
-            for (int qq = 0; qq < QPC; ++qq) {
-              const int qi = c * QPC + qq;
-              const float* wq = sW + qi * HQ;
-              float sc = 0.f;
-#pragma unroll
-              for (int jj = 0; jj < HQ; ++jj) sc = fmaf(wq[jj], fmaxf(__uint_as_float(r[qq * HQ + jj]), 0.f), sc);
-              emit(qi, sc);
-            }
-          } else {
-            const float* wq = sW + c * 32;
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) part = fmaf(wq[jj], fmaxf(__uint_as_float(r[jj]), 0.f), part);
-            if (((c + 1) * 32) % HQ == 0) {
-              emit((c * 32) / HQ, part);
-              part = 0.f;
-            }
-          }
-        }
+        const int key0 = jt * kTileKeys + quad * 32;
+        const int key = key0 + lane;
+        const uint32_t taddr =
+            tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols + split * C::COLS;
+        float sc[QW];
+        float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
+        uint32_t ra[16], rb[16];
+        ptx::tmem_ld_x16(taddr, ra);
+        ptx::tmem_wait_ld_dep16(ra);
+        drain<HQ, QW, C::NCH, 0>(taddr, wcol, sc, p0, p1, ra, rb);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }
+
+        if constexpr (FILTER) {
+          // vote-transposed append: every lane stages its QW scores, one ballot per
+          // query gives that query's passing-lane mask, and lane q appends query q's
+          // candidates in ascending key order (lists stay sorted by token index).
+          uint32_t mq = 0;
+          bool any = false;
+#pragma unroll
+          for (int q = 0; q < QW; ++q) {
+            const bool pass = key < lim_r[q] && sc[q] >= tau_r[q];
+            const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+            any |= bal != 0u;
+            if (lane == q) mq = bal;
+            stg[q * 32 + lane] = sc[q];
+          }
+          if (any) {
+            __syncwarp();
+            int pos = cnt;
+            cnt += __popc(mq);
+            while (mq) {
+              const int l = __ffs(mq) - 1;
+              mq &= mq - 1;
+              if (pos < a.cap)
+                dst[pos] = (static_cast<uint64_t>(static_cast<uint32_t>(key0 + l)) << 32) |
+                           __float_as_uint(stg[lane * 32 + l]);
+              ++pos;
+            }
+          }
+          __syncwarp();
+        } else {
+#pragma unroll
+          for (int q = 0; q < QW; ++q)
+            if (key < lim_r[q]) a.out[(int64_t)(row0 + qbase + q) * a.out_ld + key] = sc[q];
+        }
       }
       if constexpr (FILTER) {
-        if (lane < G) {
-          const int row = row0 + lane;
+        if (lane < QW) {
+          const int row = row0 + qbase + lane;
           if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = cnt;
         }
       }
-      ptx::named_bar_sync(1, 32 * kQuadrants);
+      ptx::named_bar_sync(1, EPI_THREADS);
     }
   }
 

@@ -2,217 +2,299 @@
 //
 // The reference's rule is argsort(-scores, kind="stable")[:k] then sort: the
 // k largest scores, ties to the smaller index, returned ascending.  Every
-// kernel here implements exactly that order, (score desc, index asc), with a
-// block-wide MSD radix select over monotone u32 keys (-0.0 == +0.0):
-//   1. skip the common high bits of all keys (one OR-reduction),
-//   2. 8-bit digit passes with warp-aggregated smem histograms until the k-th
-//      key v is pinned (cnt_gt keys are strictly greater),
-//   3. if the keys equal to v over-fill the budget, a second radix select on
-//      the complemented index picks the smallest indices among the ties,
-//   4. the selected indices are bitonic-sorted ascending in smem.
+// kernel here implements exactly that order, (score desc, index asc), on
+// monotone u32 keys (-0.0 == +0.0).
 //
-// misa_select_threshold  one CTA per row over the sampled scores (tau)
-// misa_select_topk       one CTA per row over the filtered candidates (staged in smem)
-// misa_select_dense      one CTA per row over a dense score row (global passes)
-// misa_merge_topk        one CTA per row over the gathered per-GPU top-k lists
+// Register selector (one CTA per row, NT threads x EPT elements in registers,
+// element e = r*NT + tid):
+//   1. the k-th largest key v is built bit by bit from the highest bit that
+//      differs across the row: v |= bit while count(key >= v|bit) >= k, each
+//      count one compare per element + a warp REDUX + one barrier — no atomics;
+//   2. if the keys equal to v over-fill the budget, the same search on the
+//      indices of the tied keys keeps the smallest ones;
+//   3. output order needs no sort: every input is a few lists already ascending
+//      by token index (the scorer appends each TMEM lane quadrant's candidates
+//      in key order; candidate / per-GPU lists are ascending by construction).
+//      One block scan of per-(round, warp) ballot counts compacts the selected
+//      elements per list; position = rank in own list + lower_bound in the others.
+//
+// misa_select_threshold  tau: j-th largest sampled score per row
+// misa_select_topk       4 per-quadrant candidate lists per row
+// misa_select_dense      a dense (optionally index-listed) row; rows too long for
+//                        registers take a global-memory radix path (exact fallback)
+// misa_merge_topk        the gathered per-GPU top-k lists of a row
 #include "common.cuh"
 #include "ptx.cuh"
 
 namespace misa {
 
-constexpr int kSelThreads = 512;
+constexpr int kMaxLists = 8;
 
-struct SelShared {
-  uint32_t hist[256];
-  uint32_t red[32];
-  int info[8];
+template <int NT>
+struct SelSh {
+  static constexpr int NW = NT / 32;
+  int cnt[2][NW];
+  uint32_t red[NW];
+  int tab[NT];  // per-(round, warp) selected counts, scanned in place
+  int wtot[NW];
+  int lst_off[kMaxLists + 1];
+  int lst_sel[kMaxLists + 1];
 };
 
-__device__ __forceinline__ uint32_t block_or(uint32_t v, SelShared& sh) {
+template <int NT>
+__device__ __forceinline__ uint32_t block_reduce_or(uint32_t v, SelSh<NT>& sh) {
   v = __reduce_or_sync(0xffffffffu, v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) sh.red[w] = v;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sh.red[w] = v;
   __syncthreads();
-  if (w == 0) {
-    uint32_t x = (l < (int)(blockDim.x >> 5)) ? sh.red[l] : 0u;
-    x = __reduce_or_sync(0xffffffffu, x);
-    if (l == 0) sh.red[0] = x;
-  }
-  __syncthreads();
-  const uint32_t r = sh.red[0];
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < SelSh<NT>::NW; ++i) r |= sh.red[i];
   __syncthreads();
   return r;
 }
 
-// Find the j-th largest (1-indexed, j <= N) among keys key_of(i), i < N.
-// Returns v; *j_rem = rank of the target among keys == v (1..cnt_eq); *cnt_eq.
-template <typename KeyFn>
-__device__ uint32_t radix_select(KeyFn key_of, int N, int j, SelShared& sh, int* j_rem_out, int* cnt_eq_out) {
-  const uint32_t first = key_of(0);
-  uint32_t diff = 0;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) diff |= key_of(i) ^ first;
-  diff = block_or(diff, sh);
+// Block-wide count of elements satisfying pred(r) (register slot r of this thread).
+template <int NT, int EPT, typename Pred>
+__device__ __forceinline__ int block_count(Pred pred, SelSh<NT>& sh, int& parity) {
+  int c = 0;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) c += pred(r) ? 1 : 0;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) sh.cnt[parity][threadIdx.x >> 5] = c;
+  __syncthreads();
+  int tot = 0;
+#pragma unroll
+  for (int i = 0; i < SelSh<NT>::NW; ++i) tot += sh.cnt[parity][i];
+  parity ^= 1;
+  return tot;
+}
+
+// Largest v such that count(val(r) >= v) >= j, over valid slots; val() >= 1 for valid.
+// Returns v and the count of values >= v (*c_ge) (values > v: *c_gt).
+template <int NT, int EPT, typename Val>
+__device__ uint32_t kth_largest(Val val, int j, SelSh<NT>& sh, int& parity, int* c_ge, int* c_gt,
+                                int min_bit = 0) {
+  uint32_t lo_or = 0, diff = 0, first = 0;
+  // common high bits of the valid values: OR of (val ^ some valid value)
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) lo_or |= val(r);
+  // a value present in the block to xor against: the block OR is not a member, so use
+  // per-bit agreement: bits set in every valid value = AND, set in any = OR.
+  uint32_t a_and = 0xffffffffu;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const uint32_t x = val(r);
+    if (x) a_and &= x;
+  }
+  const uint32_t any_or = block_reduce_or<NT>(lo_or, sh);
+  const uint32_t all_and = ~block_reduce_or<NT>(~a_and, sh);
+  diff = any_or ^ all_and;  // bits that differ across the valid values
+  first = all_and;          // bits common to all valid values (those above hi are the prefix)
+  uint32_t v;
+  int cge;
   if (diff == 0) {
-    *j_rem_out = j;
-    *cnt_eq_out = N;
-    return first;
-  }
-  int hi = 31 - __clz(diff);
-  uint32_t prefix = (hi == 31) ? 0u : (first & ~((2u << hi) - 1u));
-  int j_rem = j;
-  int cnt_eq = 0;
-  const uint32_t lane_lt = ptx::lanemask_lt();
-  (void)lane_lt;
-  while (hi >= 0) {
-    const int lo = hi >= 7 ? hi - 7 : 0;
-    const int width = hi - lo + 1;
-    const uint32_t dmask = (width == 32) ? 0xffffffffu : ((1u << width) - 1u);
-    const uint32_t mhi = (hi == 31) ? 0u : ~((2u << hi) - 1u);
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.hist[i] = 0;
-    __syncthreads();
-    // warp-uniform trip count so the aggregation below can use full-mask intrinsics
-    const int trips = (N + blockDim.x - 1) / blockDim.x;
-    for (int tr = 0; tr < trips; ++tr) {
-      const int i = tr * blockDim.x + threadIdx.x;
-      bool ok = false;
-      uint32_t d = 0;
-      if (i < N) {
-        const uint32_t k = key_of(i);
-        ok = (k & mhi) == (prefix & mhi);
-        d = (k >> lo) & dmask;
-      }
-      const uint32_t act = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        const uint32_t peers = __match_any_sync(act, d);
-        if ((__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&sh.hist[d], __popc(peers));
+    v = first;
+    cge = block_count<NT, EPT>([&](int r) { return val(r) >= v; }, sh, parity);
+  } else {
+    const int hi = 31 - __clz(diff);
+    v = (hi == 31) ? 0u : (first & ~((2u << hi) - 1u));
+    cge = -1;
+    for (int b = hi; b >= min_bit; --b) {
+      const uint32_t cand = v | (1u << b);
+      const int c = block_count<NT, EPT>([&](int r) { return val(r) >= cand; }, sh, parity);
+      if (c >= j) {
+        v = cand;
+        cge = c;
       }
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      // lane l owns bins [8l, 8l+8) counted from the top digit down
-      const int l = threadIdx.x;
-      const int nb = (int)dmask + 1;  // bins in use (<= 256)
-      uint32_t c[8];
-      uint32_t tot = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int bin = nb - 1 - (8 * l + q);
-        c[q] = bin >= 0 ? sh.hist[bin] : 0u;
-        tot += c[q];
-      }
-      uint32_t incl = tot;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-        if (l >= off) incl += y;
-      }
-      const uint32_t excl = incl - tot;
-      const bool here = (excl < (uint32_t)j_rem) && ((uint32_t)j_rem <= incl);
-      if (here) {
-        uint32_t above = excl;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if ((uint32_t)j_rem <= above + c[q]) {
-            sh.info[0] = nb - 1 - (8 * l + q);
-            sh.info[1] = (int)above;
-            sh.info[2] = (int)c[q];
-            break;
-          }
-          above += c[q];
-        }
-      }
-    }
-    __syncthreads();
-    const int dsel = sh.info[0];
-    j_rem -= sh.info[1];
-    cnt_eq = sh.info[2];
-    prefix |= (uint32_t)dsel << lo;
-    __syncthreads();
-    hi = lo - 1;
+    if (cge < 0) cge = block_count<NT, EPT>([&](int r) { return val(r) >= v; }, sh, parity);
   }
-  *j_rem_out = j_rem;
-  *cnt_eq_out = cnt_eq;
-  return prefix;
+  if (min_bit > 0) {  // approximate mode: v is a lower bound of the j-th value, counts not needed
+    *c_ge = cge;
+    *c_gt = -1;
+    return v;
+  }
+  const int cgt = (v == 0xffffffffu) ? 0 : block_count<NT, EPT>([&](int r) { return val(r) > v; }, sh, parity);
+  *c_ge = cge;
+  *c_gt = cgt;
+  return v;
 }
 
-// Selected set = keys > v, plus keys == v with index <= idx_thr.  Resolves idx_thr.
-template <typename KeyFn, typename IdxFn>
-__device__ void select_rule(KeyFn key_of, IdxFn idx_of, int N, int kk, SelShared& sh, uint32_t* v_out,
-                            int* idx_thr_out) {
-  int j_rem, cnt_eq;
-  const uint32_t v = radix_select(key_of, N, kk, sh, &j_rem, &cnt_eq);
-  int idx_thr = 0x7fffffff;
-  if (j_rem < cnt_eq) {
-    int jr2, ce2;
-    auto tie_key = [&](int i) -> uint32_t { return key_of(i) == v ? ~(uint32_t)idx_of(i) : 0u; };
-    const uint32_t v2 = radix_select(tie_key, N, j_rem, sh, &jr2, &ce2);
-    idx_thr = (int)~v2;
+// Merge path: how many of A's elements are among the first d outputs of merge(A, B)
+// (A, B ascending; token indices are unique across lists).
+__device__ __forceinline__ int merge_path(const int32_t* A, int na, const int32_t* B, int nb, int d) {
+  int lo = d - nb > 0 ? d - nb : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A[mid] < B[d - 1 - mid]) lo = mid + 1;
+    else hi = mid;
   }
-  *v_out = v;
-  *idx_thr_out = idx_thr;
+  return lo;
 }
 
-// Bitonic sort of n_pow2 u64 in smem, ascending.
-__device__ void bitonic_sort_u64(uint64_t* a, int n_pow2) {
-  for (int k = 2; k <= n_pow2; k <<= 1) {
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
-        const int ixj = i ^ jj;
-        if (ixj > i) {
-          const uint64_t x = a[i], y = a[ixj];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) {
-            a[i] = y;
-            a[ixj] = x;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__device__ __forceinline__ int next_pow2(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
-
-// Collect the selected (idx, score) pairs as u64 = idx << 32 | score_bits, sort, write.
-template <typename KeyFn, typename IdxFn>
-__device__ void collect_sorted_write(KeyFn key_of, IdxFn idx_of, int N, int kk, uint32_t v, int idx_thr,
-                                     uint64_t* buf, int* counter, int32_t* out_idx, float* out_score, int k_out) {
-  const int np2 = next_pow2(kk);
-  for (int i = threadIdx.x; i < np2; i += blockDim.x) buf[i] = ~0ull;
-  if (threadIdx.x == 0) *counter = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const uint32_t k = key_of(i);
-    const int ix = idx_of(i);
-    if (k > v || (k == v && ix <= idx_thr)) {
-      const int pos = atomicAdd(counter, 1);
-      if (pos < kk) buf[pos] = (static_cast<uint64_t>(static_cast<uint32_t>(ix)) << 32) | __float_as_uint(key_float(k));
-    }
-  }
-  __syncthreads();
-  bitonic_sort_u64(buf, np2);
-  for (int i = threadIdx.x; i < k_out; i += blockDim.x) {
-    if (i < kk) {
-      out_idx[i] = (int32_t)(buf[i] >> 32);
-      if (out_score) out_score[i] = __uint_as_float((uint32_t)buf[i]);
+// All NT threads merge A and B into D (each thread one contiguous output chunk).
+template <int NT>
+__device__ __forceinline__ void merge_pair(const int32_t* A, const float* As, int na, const int32_t* B,
+                                           const float* Bs, int nb, int32_t* D, float* Ds) {
+  const int M = na + nb;
+  const int chunk = (M + NT - 1) / NT;
+  const int d0 = min(M, (int)threadIdx.x * chunk), d1 = min(M, d0 + chunk);
+  if (d0 >= d1) return;
+  int i = merge_path(A, na, B, nb, d0), j = d0 - i;
+  for (int d = d0; d < d1; ++d) {
+    const bool take_a = j >= nb || (i < na && A[i] < B[j]);
+    if (take_a) {
+      D[d] = A[i];
+      if (Ds) Ds[d] = As[i];
+      ++i;
     } else {
-      out_idx[i] = -1;
-      if (out_score) out_score[i] = -INFINITY;
+      D[d] = B[j];
+      if (Ds) Ds[d] = Bs[j];
+      ++j;
     }
+  }
+}
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int x) {
+  int lo = 0;
+  while (n > 0) {
+    const int half = n >> 1;
+    if (a[lo + half] < x) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
+
+// Core: key[EPT]/idx[EPT] in registers (element e = r*NT + tid, key 0 = empty slot),
+// NL lists with element offsets sh.lst_off[0..NL].  Selects the kk best
+// (key desc, idx asc) and writes them ascending by index to out[0..kk), scores
+// to outs (optional), -1 padding to k_out.  cidx/csc: smem scratch of kk entries.
+template <int NT, int EPT>
+__device__ void select_ordered(const uint32_t (&key)[EPT], const int32_t (&idx)[EPT], int N, int NL, int kk,
+                               SelSh<NT>& sh, int32_t* cidx, float* csc, int32_t* out, float* outs, int k_out) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int parity = 0;
+  uint32_t v = 0;
+  int thr = 0x7fffffff;
+  if (kk < N) {
+    int cge, cgt;
+    v = kth_largest<NT, EPT>([&](int r) { return key[r]; }, kk, sh, parity, &cge, &cgt);
+    const int need = kk - cgt;    // ties to keep
+    const int ties = cge - cgt;   // keys == v
+    if (need < ties) {
+      // keep the `need` smallest indices among the ties: (ties-need+1)-th largest of ~idx
+      int c2, c3;
+      const uint32_t t2 = kth_largest<NT, EPT>(
+          [&](int r) { return (key[r] == v) ? ~static_cast<uint32_t>(idx[r]) : 0u; }, need, sh, parity, &c2, &c3);
+      thr = static_cast<int>(~t2);
+    }
+  }
+  // ordered compaction: ballots per (round, warp) -> block scan -> ranks
+  auto selected = [&](int r) -> bool {
+    return key[r] != 0u && (kk >= N || key[r] > v || (key[r] == v && idx[r] <= thr));
+  };
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const uint32_t b = __ballot_sync(0xffffffffu, selected(r));
+    if (lane == 0) sh.tab[r * NW + w] = __popc(b);
+  }
+  __syncthreads();
+  {
+    // exclusive scan of the EPT*NW (<= NT) counts
+    constexpr int TS = EPT * NW;
+    const int x = tid < TS ? sh.tab[tid] : 0;
+    int inc = x;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += y;
+    }
+    if (lane == 31) sh.wtot[w] = inc;
+    __syncthreads();
+    int pre = 0;
+    for (int i = 0; i < w; ++i) pre += sh.wtot[i];
+    if (tid < TS) sh.tab[tid] = pre + inc - x;
+    __syncthreads();
+  }
+  const uint32_t lt = ptx::lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int e = r * NT + tid;
+    const bool sel = selected(r);
+    const uint32_t b = __ballot_sync(0xffffffffu, sel);
+    const int rank = sh.tab[r * NW + w] + __popc(b & lt);
+    for (int l = 0; l <= NL; ++l)
+      if (sh.lst_off[l] == e && e < N) sh.lst_sel[l] = rank;
+    if (sel) {
+      cidx[rank] = idx[r];
+      if (csc) csc[rank] = key_float(key[r]);
+    }
+  }
+  if (tid == 0)
+    for (int l = 0; l <= NL; ++l)
+      if (sh.lst_off[l] >= N) sh.lst_sel[l] = kk;
+  __syncthreads();
+  // pairwise merge-path rounds over the NL sorted runs; the last round writes `out`
+  int32_t* src = cidx;
+  float* srcs = csc;
+  int32_t* tmp = cidx + k_out;
+  float* tmps = csc ? csc + k_out : nullptr;
+  int runs = NL;
+  while (runs > 2) {
+    for (int p = 0; p + 1 < runs; p += 2) {
+      const int a0 = sh.lst_sel[p], a1 = sh.lst_sel[p + 1], b1 = sh.lst_sel[p + 2];
+      merge_pair<NT>(src + a0, srcs ? srcs + a0 : nullptr, a1 - a0, src + a1, srcs ? srcs + a1 : nullptr, b1 - a1,
+                     tmp + a0, tmps ? tmps + a0 : nullptr);
+    }
+    if (runs & 1) {
+      for (int i = sh.lst_sel[runs - 1] + tid; i < sh.lst_sel[runs]; i += NT) {
+        tmp[i] = src[i];
+        if (tmps) tmps[i] = srcs[i];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int nr = 0;
+      for (int p = 0; p < runs; p += 2) sh.lst_sel[nr++] = sh.lst_sel[p];
+      sh.lst_sel[nr] = kk;
+    }
+    runs = (runs + 1) / 2;
+    int32_t* t1 = src;
+    src = tmp;
+    tmp = t1;
+    float* t2 = srcs;
+    srcs = tmps;
+    tmps = t2;
+    __syncthreads();
+  }
+  if (runs == 2) {
+    const int a0 = sh.lst_sel[0], a1 = sh.lst_sel[1], b1 = sh.lst_sel[2];
+    merge_pair<NT>(src + a0, srcs ? srcs + a0 : nullptr, a1 - a0, src + a1, srcs ? srcs + a1 : nullptr, b1 - a1,
+                   out + a0, outs ? outs + a0 : nullptr);
+  } else {
+    for (int i = tid; i < kk; i += NT) {
+      out[i] = src[i];
+      if (outs) outs[i] = srcs[i];
+    }
+  }
+  for (int i = kk + tid; i < k_out; i += NT) {
+    out[i] = -1;
+    if (outs) outs[i] = -INFINITY;
   }
 }
 
 // ---------------------------------------------------------------- tau ----
-__global__ void __launch_bounds__(kSelThreads) threshold_kernel(const float* __restrict__ s, int64_t ld,
-                                                                const int32_t* __restrict__ prefix_len, int T,
-                                                                int stride, int k, float beta, int64_t append_all,
-                                                                float* __restrict__ tau) {
-  __shared__ SelShared sh;
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__ s, int64_t ld,
+                                                       const int32_t* __restrict__ prefix_len, int stride, int k,
+                                                       float beta, int64_t append_all, float* __restrict__ tau) {
+  __shared__ SelSh<NT> sh;
   const int t = blockIdx.x;
   const int n = prefix_len[t];
   if (n <= append_all || n <= k) {
@@ -221,85 +303,202 @@ __global__ void __launch_bounds__(kSelThreads) threshold_kernel(const float* __r
   }
   const int m = (n + stride - 1) / stride;
   long long jj = (long long)ceilf(beta * (float)k * (float)m / (float)n);
-  if (jj < 1) jj = 1;
-  if (jj > m) jj = m;
+  jj = jj < 1 ? 1 : (jj > m ? m : jj);
   const float* row = s + (int64_t)t * ld;
-  auto key_of = [&](int i) -> uint32_t { return float_key(row[i]); };
-  int jr, ce;
-  const uint32_t v = radix_select(key_of, m, (int)jj, sh, &jr, &ce);
+  uint32_t key[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int e = r * NT + threadIdx.x;
+    key[r] = e < m ? float_key(row[e]) : 0u;
+  }
+  int parity = 0, cge, cgt;
+  // tau only has to be a lower bound of the j-th sampled score: resolve the sign, all 8
+  // exponent bits and 10 mantissa bits (key bits 31..13), round the rest down — at most
+  // 2^-10 relative below the exact value (a few more candidates, never fewer)
+  const uint32_t v =
+      kth_largest<NT, EPT>([&](int r) { return key[r]; }, (int)jj, sh, parity, &cge, &cgt, /*min_bit=*/13);
   if (threadIdx.x == 0) tau[t] = key_float(v);
 }
 
 // -------------------------------------------------- candidates -> top-k ----
-__global__ void __launch_bounds__(kSelThreads) topk_kernel(const uint64_t* __restrict__ cand,
-                                                           const int32_t* __restrict__ cand_count, int cap,
-                                                           const int32_t* __restrict__ prefix_len, int T, int k,
-                                                           int32_t* __restrict__ topk, int64_t topk_ld,
-                                                           float* __restrict__ topk_scores, int32_t* __restrict__ flags,
-                                                           int staged_cap) {
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) topk_kernel(const uint64_t* __restrict__ cand,
+                                                  const int32_t* __restrict__ cand_count, int cap,
+                                                  const int32_t* __restrict__ prefix_len, int k,
+                                                  int32_t* __restrict__ topk, int64_t topk_ld,
+                                                  float* __restrict__ topk_scores, int32_t* __restrict__ flags) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  __shared__ SelShared sh;
-  __shared__ int counter;
+  __shared__ SelSh<NT> sh;
   const int t = blockIdx.x;
   const int n = prefix_len[t];
   int32_t* out = topk + (int64_t)t * topk_ld;
   float* outs = topk_scores ? topk_scores + (int64_t)t * topk_ld : nullptr;
   if (n <= k) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73)
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    for (int i = threadIdx.x; i < k; i += NT) {
       out[i] = i < n ? i : -1;
       if (outs && i >= n) outs[i] = -INFINITY;
     }
     if (threadIdx.x == 0 && flags) flags[t] = 0;
     return;
   }
-  int cnt[kQuadrants];
-  int total = 0;
+  int cnt[kQuadrants], off[kQuadrants + 1];
   bool overflow = false;
+  off[0] = 0;
 #pragma unroll
   for (int q = 0; q < kQuadrants; ++q) {
     cnt[q] = cand_count[(int64_t)t * kQuadrants + q];
     overflow |= cnt[q] > cap;
-    total += cnt[q] < cap ? cnt[q] : cap;
+    off[q + 1] = off[q] + (cnt[q] < cap ? cnt[q] : cap);
   }
-  const int kk = k;  // n > k here
-  if (overflow || total < kk || total > staged_cap) {
-    for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = -1;
-    if (threadIdx.x == 0 && flags) flags[t] = overflow || total > staged_cap ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
+  const int total = off[kQuadrants];
+  if (overflow || total < k || total > NT * EPT) {
+    for (int i = threadIdx.x; i < k; i += NT) out[i] = -1;
+    if (threadIdx.x == 0 && flags)
+      flags[t] = (overflow || total > NT * EPT) ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
     return;
   }
-  uint32_t* skey = reinterpret_cast<uint32_t*>(dsm);
-  int32_t* sidx = reinterpret_cast<int32_t*>(dsm + (size_t)staged_cap * 4);
-  uint64_t* buf = reinterpret_cast<uint64_t*>(dsm + (size_t)staged_cap * 8);
-  int off = 0;
+  if (threadIdx.x <= kQuadrants) sh.lst_off[threadIdx.x] = off[threadIdx.x];
+  uint32_t key[EPT];
+  int32_t idx[EPT];
+  // all loads of a thread in flight before any use (candidate = key << 32 | score bits)
 #pragma unroll
-  for (int q = 0; q < kQuadrants; ++q) {
-    const uint64_t* src = cand + ((int64_t)t * kQuadrants + q) * cap;
-    for (int i = threadIdx.x; i < cnt[q]; i += blockDim.x) {
-      const uint64_t c = src[i];
-      skey[off + i] = float_key(__uint_as_float((uint32_t)c));
-      sidx[off + i] = (int32_t)(c >> 32);
+  for (int r = 0; r < EPT; ++r) {
+    const int e = r * NT + threadIdx.x;
+    uint2 rw = make_uint2(0u, 0u);
+    if (e < total) {
+      int q = 0;
+#pragma unroll
+      for (int qq = 1; qq < kQuadrants; ++qq) q += e >= off[qq];
+      rw = *reinterpret_cast<const uint2*>(cand + ((int64_t)t * kQuadrants + q) * cap + (e - off[q]));
     }
-    off += cnt[q];
+    key[r] = rw.x;
+    idx[r] = static_cast<int32_t>(rw.y);
+  }
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int e = r * NT + threadIdx.x;
+    key[r] = e < total ? float_key(__uint_as_float(key[r])) : 0u;
   }
   __syncthreads();
-  auto key_of = [&](int i) -> uint32_t { return skey[i]; };
-  auto idx_of = [&](int i) -> int { return sidx[i]; };
-  uint32_t v;
-  int idx_thr;
-  select_rule(key_of, idx_of, total, kk, sh, &v, &idx_thr);
-  collect_sorted_write(key_of, idx_of, total, kk, v, idx_thr, buf, &counter, out, outs, k);
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
+  float* csc = reinterpret_cast<float*>(dsm + (size_t)k * 8);
+  select_ordered<NT, EPT>(key, idx, total, kQuadrants, k, sh, cidx, outs ? csc : nullptr, out, outs, k);
   if (threadIdx.x == 0 && flags) flags[t] = 0;
 }
 
 // ------------------------------------------------------- dense rows ----
-__global__ void __launch_bounds__(kSelThreads) dense_kernel(const float* __restrict__ s, int64_t ld,
-                                                            const int32_t* __restrict__ idx, int64_t idx_ld,
-                                                            const int32_t* __restrict__ row_len,
-                                                            const int32_t* __restrict__ rows, int k,
-                                                            int32_t* __restrict__ topk, int64_t topk_ld,
-                                                            float* __restrict__ topk_scores) {
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) dense_reg_kernel(const float* __restrict__ s, int64_t ld,
+                                                       const int32_t* __restrict__ idx, int64_t idx_ld,
+                                                       const int32_t* __restrict__ row_len,
+                                                       const int32_t* __restrict__ rows, int k,
+                                                       int32_t* __restrict__ topk, int64_t topk_ld,
+                                                       float* __restrict__ topk_scores) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  __shared__ SelShared sh;
+  __shared__ SelSh<NT> sh;
+  const int rr = rows ? rows[blockIdx.x] : blockIdx.x;
+  const int n = row_len[rr];
+  const float* row = s + (int64_t)rr * ld;
+  const int32_t* irow = idx ? idx + (int64_t)rr * idx_ld : nullptr;
+  int32_t* out = topk + (int64_t)rr * topk_ld;
+  float* outs = topk_scores ? topk_scores + (int64_t)rr * topk_ld : nullptr;
+  const int kk = n < k ? n : k;
+  uint32_t key[EPT];
+  int32_t ix[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int e = r * NT + threadIdx.x;
+    key[r] = e < n ? float_key(row[e]) : 0u;
+    ix[r] = e < n ? (irow ? irow[e] : e) : 0x7fffffff;
+  }
+  if (threadIdx.x == 0) {
+    sh.lst_off[0] = 0;
+    sh.lst_off[1] = n;
+  }
+  __syncthreads();
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
+  float* csc = reinterpret_cast<float*>(dsm + (size_t)k * 8);
+  if (kk <= 0) {
+    for (int i = threadIdx.x; i < k; i += NT) {
+      out[i] = -1;
+      if (outs) outs[i] = -INFINITY;
+    }
+    return;
+  }
+  select_ordered<NT, EPT>(key, ix, n, 1, kk, sh, cidx, outs ? csc : nullptr, out, outs, k);
+}
+
+// Global path for rows longer than the register capacity (exact fallback): MSB radix
+// passes over global memory with smem histograms, then rank-by-comparison ordering.
+constexpr int kGlbThreads = 256;
+struct GlbShared {
+  uint32_t hist[256];
+  uint32_t red[kGlbThreads / 32];
+  int info[4];
+};
+
+template <typename KeyFn>
+__device__ uint32_t glb_radix_select(KeyFn key_of, int N, int j, GlbShared& sh, int* j_rem_out, int* cnt_eq_out) {
+  const uint32_t first = key_of(0);
+  uint32_t diff = 0;
+  for (int i = threadIdx.x; i < N; i += kGlbThreads) diff |= key_of(i) ^ first;
+  diff = __reduce_or_sync(0xffffffffu, diff);
+  if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = diff;
+  __syncthreads();
+  diff = 0;
+  for (int i = 0; i < kGlbThreads / 32; ++i) diff |= sh.red[i];
+  __syncthreads();
+  if (diff == 0) {
+    *j_rem_out = j;
+    *cnt_eq_out = N;
+    return first;
+  }
+  int hi = 31 - __clz(diff);
+  uint32_t prefix = (hi == 31) ? 0u : (first & ~((2u << hi) - 1u));
+  int j_rem = j, cnt_eq = 0;
+  while (hi >= 0) {
+    const int lo = hi >= 7 ? hi - 7 : 0;
+    const uint32_t dmask = (1u << (hi - lo + 1)) - 1u;
+    const uint32_t mhi = (hi == 31) ? 0u : ~((2u << hi) - 1u);
+    for (int i = threadIdx.x; i < 256; i += kGlbThreads) sh.hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += kGlbThreads) {
+      const uint32_t k = key_of(i);
+      if ((k & mhi) == (prefix & mhi)) atomicAdd(&sh.hist[(k >> lo) & dmask], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t above = 0;
+      for (int d = (int)dmask; d >= 0; --d) {
+        if ((uint32_t)j_rem <= above + sh.hist[d]) {
+          sh.info[0] = d;
+          sh.info[1] = (int)above;
+          sh.info[2] = (int)sh.hist[d];
+          break;
+        }
+        above += sh.hist[d];
+      }
+    }
+    __syncthreads();
+    j_rem -= sh.info[1];
+    cnt_eq = sh.info[2];
+    prefix |= (uint32_t)sh.info[0] << lo;
+    __syncthreads();
+    hi = lo - 1;
+  }
+  *j_rem_out = j_rem;
+  *cnt_eq_out = cnt_eq;
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kGlbThreads) dense_global_kernel(const float* __restrict__ s, int64_t ld,
+                                                                   const int32_t* __restrict__ idx, int64_t idx_ld,
+                                                                   const int32_t* __restrict__ row_len,
+                                                                   const int32_t* __restrict__ rows, int k,
+                                                                   int32_t* __restrict__ topk, int64_t topk_ld,
+                                                                   float* __restrict__ topk_scores) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ GlbShared sh;
   __shared__ int counter;
   const int r = rows ? rows[blockIdx.x] : blockIdx.x;
   const int n = row_len[r];
@@ -307,82 +506,170 @@ __global__ void __launch_bounds__(kSelThreads) dense_kernel(const float* __restr
   const int32_t* irow = idx ? idx + (int64_t)r * idx_ld : nullptr;
   int32_t* out = topk + (int64_t)r * topk_ld;
   float* outs = topk_scores ? topk_scores + (int64_t)r * topk_ld : nullptr;
-  uint64_t* buf = reinterpret_cast<uint64_t*>(dsm);
   auto key_of = [&](int i) -> uint32_t { return float_key(row[i]); };
   auto idx_of = [&](int i) -> int { return irow ? irow[i] : i; };
   const int kk = n < k ? n : k;
-  if (kk <= 0) {
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
-      out[i] = -1;
-      if (outs) outs[i] = -INFINITY;
-    }
-    return;
-  }
   uint32_t v = 0;
-  int idx_thr = 0x7fffffff;
-  if (kk < n) select_rule(key_of, idx_of, n, kk, sh, &v, &idx_thr);
-  collect_sorted_write(key_of, idx_of, n, kk, v, idx_thr, buf, &counter, out, outs, k);
+  int thr = 0x7fffffff;
+  if (kk > 0 && kk < n) {
+    int j_rem, cnt_eq;
+    v = glb_radix_select(key_of, n, kk, sh, &j_rem, &cnt_eq);
+    if (j_rem < cnt_eq) {
+      int jr2, ce2;
+      auto tie_key = [&](int i) -> uint32_t { return key_of(i) == v ? ~(uint32_t)idx_of(i) : 0u; };
+      thr = (int)~glb_radix_select(tie_key, n, j_rem, sh, &jr2, &ce2);
+    }
+  }
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
+  float* csc = reinterpret_cast<float*>(dsm + (size_t)k * 4);
+  if (threadIdx.x == 0) counter = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += kGlbThreads) {
+    const uint32_t kv = key_of(i);
+    if (kk > 0 && (kk >= n || kv > v || (kv == v && idx_of(i) <= thr))) {
+      const int p = atomicAdd(&counter, 1);
+      if (p < kk) {
+        cidx[p] = idx_of(i);
+        csc[p] = key_float(kv);
+      }
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < kk; p += kGlbThreads) {
+    const int x = cidx[p];
+    int pos = 0;
+    for (int q = 0; q < kk; ++q) pos += cidx[q] < x;
+    out[pos] = x;
+    if (outs) outs[pos] = csc[p];
+  }
+  for (int i = kk + threadIdx.x; i < k; i += kGlbThreads) {
+    out[i] = -1;
+    if (outs) outs[i] = -INFINITY;
+  }
 }
 
 // -------------------------------------------------- multi-GPU merge ----
-__global__ void __launch_bounds__(kSelThreads) merge_kernel(const float* __restrict__ ps, const int32_t* __restrict__ pi,
-                                                            int n_parts, int64_t part_stride, int k_in, int k,
-                                                            int32_t* __restrict__ topk, int64_t topk_ld) {
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) merge_kernel(const float* __restrict__ ps, const int32_t* __restrict__ pi,
+                                                   int n_parts, int64_t part_stride, int k_in, int k,
+                                                   int32_t* __restrict__ topk, int64_t topk_ld) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  __shared__ SelShared sh;
-  __shared__ int counter;
+  __shared__ SelSh<NT> sh;
   const int t = blockIdx.x;
-  const int N = n_parts * k_in;
-  auto at = [&](int i) -> int64_t { return (int64_t)(i / k_in) * part_stride + (int64_t)t * k_in + (i % k_in); };
-  // -1 entries (short local lists) rank below every real candidate
-  auto key_of = [&](int i) -> uint32_t { return pi[at(i)] < 0 ? 0u : float_key(ps[at(i)]); };
-  auto idx_of = [&](int i) -> int { const int x = pi[at(i)]; return x < 0 ? 0x7fffffff : x; };
-  int valid = 0;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) valid += pi[at(i)] >= 0;
-  valid = __reduce_add_sync(0xffffffffu, valid);
-  __shared__ int vsum;
-  if (threadIdx.x == 0) vsum = 0;
+  // each part's list is ascending with -1 padding at the end; its valid prefix is a list
+  if (threadIdx.x < 32) {
+    int acc = 0;
+    for (int p = 0; p < n_parts; ++p) {
+      const int32_t* pidx = pi + p * part_stride + (int64_t)t * k_in;
+      int valid = 0;
+      for (int i = threadIdx.x; i < k_in; i += 32) valid += pidx[i] >= 0;
+      valid = __reduce_add_sync(0xffffffffu, valid);
+      if (threadIdx.x == 0) sh.lst_off[p] = acc;
+      acc += valid;
+    }
+    if (threadIdx.x == 0) sh.lst_off[n_parts] = acc;
+  }
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) atomicAdd(&vsum, valid);
-  __syncthreads();
-  const int kk = vsum < k ? vsum : k;
+  const int N = sh.lst_off[n_parts];
+  uint32_t key[EPT];
+  int32_t ix[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int e = r * NT + threadIdx.x;
+    key[r] = 0u;
+    ix[r] = 0x7fffffff;
+    if (e < N) {
+      int p = 0;
+      while (p + 1 < n_parts && e >= sh.lst_off[p + 1]) ++p;
+      const int64_t at = p * part_stride + (int64_t)t * k_in + (e - sh.lst_off[p]);
+      key[r] = float_key(ps[at]);
+      ix[r] = pi[at];
+    }
+  }
   int32_t* out = topk + (int64_t)t * topk_ld;
-  uint64_t* buf = reinterpret_cast<uint64_t*>(dsm);
+  const int kk = N < k ? N : k;
   if (kk <= 0) {
-    for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = -1;
+    for (int i = threadIdx.x; i < k; i += NT) out[i] = -1;
     return;
   }
-  uint32_t v = 0;
-  int idx_thr = 0x7fffffff;
-  if (kk < vsum) {
-    select_rule(key_of, idx_of, N, kk, sh, &v, &idx_thr);
-  } else {
-    v = 1u;  // every valid entry (key >= 1 since real keys are never 0) is kept
-    idx_thr = 0x7ffffffe;
-  }
-  collect_sorted_write(key_of, idx_of, N, kk, v, idx_thr, buf, &counter, out, nullptr, k);
-}
-
-static size_t sort_bytes(int k) {
-  size_t p = 1;
-  while ((int)p < k) p <<= 1;
-  return p * 8;
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
+  select_ordered<NT, EPT>(key, ix, N, n_parts, kk, sh, cidx, nullptr, out, nullptr, k);
 }
 
 }  // namespace misa
 
 using namespace misa;
 
+namespace {
+// register-capacity configurations: (threads, elements per thread)
+template <template <int, int> class Launch, typename... Args>
+int dispatch_capacity(int64_t n, cudaStream_t st, Args... args) {
+  if (n <= 256 * 8) return Launch<256, 8>::go(st, args...);
+  if (n <= 256 * 16) return Launch<256, 16>::go(st, args...);
+  if (n <= 256 * 24) return Launch<256, 24>::go(st, args...);
+  if (n <= 256 * 32) return Launch<256, 32>::go(st, args...);
+  if (n <= 512 * 32) return Launch<512, 32>::go(st, args...);
+  return -100;  // caller falls back
+}
+
+template <int NT, int EPT>
+struct ThresholdL {
+  static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
+                float beta, int64_t aa, float* tau) {
+    threshold_kernel<NT, EPT><<<(unsigned)T, NT, 0, st>>>(s, ld, pl, stride, k, beta, aa, tau);
+    MISA_LAUNCH_CHECK();
+    return MISA_OK;
+  }
+};
+
+template <int NT, int EPT>
+struct TopkL {
+  static int go(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl, int64_t T,
+                int k, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
+    const size_t bytes = (size_t)k * 16;
+    MISA_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    topk_kernel<NT, EPT><<<(unsigned)T, NT, bytes, st>>>(cand, cc, cap, pl, k, topk, ld, ts, flags);
+    MISA_LAUNCH_CHECK();
+    return MISA_OK;
+  }
+};
+
+template <int NT, int EPT>
+struct DenseL {
+  static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* idx, int64_t idx_ld,
+                const int32_t* row_len, const int32_t* rows, int64_t n_rows, int k, int32_t* topk, int64_t tld,
+                float* ts) {
+    const size_t bytes = (size_t)k * 16;
+    MISA_CUDA_TRY(
+        cudaFuncSetAttribute(dense_reg_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    dense_reg_kernel<NT, EPT><<<(unsigned)n_rows, NT, bytes, st>>>(s, ld, idx, idx_ld, row_len, rows, k, topk, tld, ts);
+    MISA_LAUNCH_CHECK();
+    return MISA_OK;
+  }
+};
+
+template <int NT, int EPT>
+struct MergeL {
+  static int go(cudaStream_t st, const float* ps, const int32_t* pi, int n_parts, int64_t stride, int64_t T, int k_in,
+                int k, int32_t* topk, int64_t ld) {
+    const size_t bytes = (size_t)k * 8;
+    MISA_CUDA_TRY(cudaFuncSetAttribute(merge_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    merge_kernel<NT, EPT><<<(unsigned)T, NT, bytes, st>>>(ps, pi, n_parts, stride, k_in, k, topk, ld);
+    MISA_LAUNCH_CHECK();
+    return MISA_OK;
+  }
+};
+}  // namespace
+
 extern "C" int misa_select_threshold(const float* sample_scores, int64_t ld, const int32_t* prefix_len,
                                      int64_t n_rows, int key_stride, int k, float beta, int64_t append_all_len,
                                      float* tau, void* stream) {
   MISA_REQUIRE(sample_scores && prefix_len && tau, "null pointer");
   MISA_REQUIRE(k >= 1 && key_stride >= 1 && beta > 0.f && n_rows >= 1, "bad threshold arguments");
-  threshold_kernel<<<(unsigned)n_rows, kSelThreads, 0, as_stream(stream)>>>(sample_scores, ld, prefix_len,
-                                                                            (int)n_rows, key_stride, k, beta,
-                                                                            append_all_len, tau);
-  MISA_LAUNCH_CHECK();
-  return MISA_OK;
+  const int rc = dispatch_capacity<ThresholdL>(ld, as_stream(stream), sample_scores, ld, prefix_len, n_rows,
+                                               key_stride, k, beta, append_all_len, tau);
+  MISA_REQUIRE(rc != -100, "sample row length %lld exceeds the register selector (16384)", (long long)ld);
+  return rc;
 }
 
 extern "C" int misa_select_topk(const uint64_t* cand, const int32_t* cand_count, int cap, const int32_t* prefix_len,
@@ -390,20 +677,10 @@ extern "C" int misa_select_topk(const uint64_t* cand, const int32_t* cand_count,
                                 int32_t* flags, void* stream) {
   MISA_REQUIRE(cand && cand_count && prefix_len && topk, "null pointer");
   MISA_REQUIRE(k >= 1 && cap >= 1 && topk_ld >= k && n_rows >= 1, "bad top-k arguments");
-  // stage up to 4*cap candidates (keys + indices) plus the sort buffer in smem
-  int staged_cap = 4 * cap;
-  size_t bytes = (size_t)staged_cap * 8 + sort_bytes(k);
-  const size_t limit = 200 * 1024;
-  if (bytes > limit) {
-    staged_cap = (int)((limit - sort_bytes(k)) / 8);
-    bytes = (size_t)staged_cap * 8 + sort_bytes(k);
-  }
-  MISA_REQUIRE(staged_cap >= k, "k=%d too large for the staged selector", k);
-  MISA_CUDA_TRY(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  topk_kernel<<<(unsigned)n_rows, kSelThreads, bytes, as_stream(stream)>>>(
-      cand, cand_count, cap, prefix_len, (int)n_rows, k, topk, topk_ld, topk_scores, flags, staged_cap);
-  MISA_LAUNCH_CHECK();
-  return MISA_OK;
+  MISA_REQUIRE((int64_t)kQuadrants * cap <= 512 * 32, "candidate capacity %d exceeds the register selector", cap);
+  MISA_REQUIRE((size_t)k * 16 <= 200 * 1024, "k too large");
+  return dispatch_capacity<TopkL>((int64_t)kQuadrants * cap, as_stream(stream), cand, cand_count, cap, prefix_len,
+                                  n_rows, k, topk, topk_ld, topk_scores, flags);
 }
 
 extern "C" int misa_select_dense(const float* scores, int64_t ld, const int32_t* idx, int64_t idx_ld,
@@ -411,12 +688,16 @@ extern "C" int misa_select_dense(const float* scores, int64_t ld, const int32_t*
                                  int64_t topk_ld, float* topk_scores, void* stream) {
   MISA_REQUIRE(scores && row_len && topk, "null pointer");
   MISA_REQUIRE(k >= 1 && topk_ld >= k, "bad k");
+  MISA_REQUIRE((size_t)k * 16 <= 200 * 1024, "k too large");
   if (n_rows <= 0) return MISA_OK;
-  const size_t bytes = sort_bytes(k);
-  MISA_REQUIRE(bytes <= 200 * 1024, "k too large");
-  MISA_CUDA_TRY(cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  dense_kernel<<<(unsigned)n_rows, kSelThreads, bytes, as_stream(stream)>>>(scores, ld, idx, idx_ld, row_len, rows, k,
-                                                                            topk, topk_ld, topk_scores);
+  cudaStream_t st = as_stream(stream);
+  int rc = dispatch_capacity<DenseL>(ld, st, scores, ld, idx, idx_ld, row_len, rows, n_rows, k, topk, topk_ld,
+                                     topk_scores);
+  if (rc != -100) return rc;
+  const size_t gb = (size_t)k * 8;
+  MISA_CUDA_TRY(cudaFuncSetAttribute(dense_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb));
+  dense_global_kernel<<<(unsigned)n_rows, kGlbThreads, gb, st>>>(scores, ld, idx, idx_ld, row_len, rows, k, topk,
+                                                                 topk_ld, topk_scores);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }
@@ -424,13 +705,10 @@ extern "C" int misa_select_dense(const float* scores, int64_t ld, const int32_t*
 extern "C" int misa_merge_topk(const float* part_scores, const int32_t* part_idx, int n_parts, int64_t part_stride,
                                int64_t n_rows, int k_in, int k, int32_t* topk, int64_t topk_ld, void* stream) {
   MISA_REQUIRE(part_scores && part_idx && topk, "null pointer");
-  MISA_REQUIRE(n_parts >= 1 && k_in >= 1 && k >= 1 && topk_ld >= k, "bad merge arguments");
+  MISA_REQUIRE(n_parts >= 1 && n_parts <= kMaxLists && k_in >= 1 && k >= 1 && topk_ld >= k, "bad merge arguments");
   if (n_rows <= 0) return MISA_OK;
-  const size_t bytes = sort_bytes(k);
-  MISA_REQUIRE(bytes <= 200 * 1024, "k too large");
-  MISA_CUDA_TRY(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  merge_kernel<<<(unsigned)n_rows, kSelThreads, bytes, as_stream(stream)>>>(part_scores, part_idx, n_parts,
-                                                                            part_stride, k_in, k, topk, topk_ld);
-  MISA_LAUNCH_CHECK();
-  return MISA_OK;
+  const int rc = dispatch_capacity<MergeL>((int64_t)n_parts * k_in, as_stream(stream), part_scores, part_idx,
+                                           n_parts, part_stride, n_rows, k_in, k, topk, topk_ld);
+  MISA_REQUIRE(rc != -100, "n_parts*k_in exceeds the register selector");
+  return rc;
 }

@@ -231,6 +231,21 @@ class IndexerEngine:
         return self._cached(key, make)
 
     # ----------------------------------------------------------- stages
+    def selector_params(self, k: int, L: int) -> tuple[int, float, int]:
+        """(sample stride, beta, per-quadrant candidate capacity) of the fused top-k.
+
+        tau is the j-th largest score on a 1/stride key sample, j = beta*k/stride, so about
+        beta*k keys pass; its relative spread is ~1/sqrt(j).  Capacity is 1.5x the expected
+        per-quadrant count (>= 5 sigma), and rows with n <= 4*cap keep every key.
+        """
+        if k < 4096:
+            stride, beta = self.stride, (self.beta or 2.0)
+        else:
+            stride, beta = max(1, self.stride // 2), (self.beta or 1.3)
+        stride = max(stride, -(-L // 16384))  # the threshold selector holds <= 16384 samples per row
+        cap = int(math.ceil(1.5 * beta * k / 4 / 32)) * 32
+        return stride, beta, cap
+
     def pool(self, x: PreparedInputs):
         """K1: in-block prefix sums + pooled planes."""
         nf = x.L // self.B
@@ -270,29 +285,27 @@ class IndexerEngine:
                tag: str = "sel") -> int:
         """Fused streaming top-k over the given head set (None = all heads). Returns #fallback rows."""
         dev = x.keys.device
-        beta = self.beta if self.beta is not None else (2.0 if k < 4096 else 1.5)
-        cap = max(64, int(math.ceil(beta * k / 2)))        # per TMEM quadrant; total 4*cap
-        cap = (cap + 7) // 8 * 8
+        stride, beta, cap = self.selector_params(k, x.L)
         append_all = 4 * cap
         G = 256 // hq
         stream = self._stream()
         ckey = x.causal_key or x.prefix_host.tobytes()
-        s_items, s_tiles = self._dev_list(("samp", ckey, G, self.stride, append_all),
-                                          lambda: self.group_items(x.prefix_host, G, self.stride, append_all), dev)
+        s_items, s_tiles = self._dev_list(("samp", ckey, G, stride, append_all),
+                                          lambda: self.group_items(x.prefix_host, G, stride, append_all), dev)
         f_items, f_tiles = self._dev_list(("filt", ckey, G, k),
                                           lambda: self.group_items(x.prefix_host, G, 1, k), dev)
-        Ls = (x.L + self.stride - 1) // self.stride
+        Ls = (x.L + stride - 1) // stride
         tau = self._buf(tag + "_tau", (x.T,), torch.float32, dev)
         if s_items.numel():
             samp = self._buf(tag + "_samp", (x.T, Ls), torch.float32, dev)
             self._mark(tag + ":sample")
-            _lib.call("misa_score_materialize", _ptr(x.keys), x.L, self.stride, x.D, _ptr(x.queries), _ptr(x.weights),
+            _lib.call("misa_score_materialize", _ptr(x.keys), x.L, stride, x.D, _ptr(x.queries), _ptr(x.weights),
                       x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(s_items), _ptr(s_tiles), s_items.numel(),
                       _ptr(samp), Ls, stream)
         else:
             samp = self._buf(tag + "_samp", (1, 1), torch.float32, dev)
         self._mark(tag + ":threshold")
-        _lib.call("misa_select_threshold", _ptr(samp), Ls, _ptr(x.prefix), x.T, self.stride, k, float(beta),
+        _lib.call("misa_select_threshold", _ptr(samp), Ls, _ptr(x.prefix), x.T, stride, k, float(beta),
                   append_all, _ptr(tau), stream)
         cand = self._buf(tag + "_cand", (x.T * 4 * cap,), torch.int64, dev)
         cnt = self._buf(tag + "_cnt", (x.T * 4,), torch.int32, dev)

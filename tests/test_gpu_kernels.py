@@ -262,7 +262,11 @@ def test_merge_topk():
     torch.manual_seed(6)
     T, k, parts = 33, 40, 3
     s = (torch.randn(parts, T, k, device="cuda") * 4).round()  # ties across parts
-    idx = torch.stack([torch.randperm(10000, device="cuda")[: T * k].view(T, k) for _ in range(parts)]).int()
+    # key shards are disjoint across GPUs: draw every part's indices from one permutation
+    idx = torch.randperm(30000, device="cuda")[: parts * T * k].view(parts, T, k).int()
+    # per-GPU lists arrive ascending by index (local top-k output), -1 padded at the end
+    idx, order = idx.sort(dim=-1)
+    s = torch.gather(s, -1, order)
     idx[1, 0, 5:] = -1
     out = torch.empty(T, k, dtype=torch.int32, device="cuda")
     _lib().call("misa_merge_topk", _p(s), _p(idx), parts, T * k, T, k, k, _p(out), k, _stream())
