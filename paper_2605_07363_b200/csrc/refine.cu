@@ -2,18 +2,22 @@
 //
 // Row t re-scores its k' coarse candidates with ALL H heads:
 //   out[t][i] = sum_j w_{t,j} ReLU(q_{t,j} . k_{cand[t][i]})
-// The A operand is a gather of candidate key rows: TMA tile::gather4 moves four
-// arbitrary 128-byte rows per instruction straight into the 128-B-swizzled
-// K-major layout the UMMA descriptor expects (box {64, 1}).  B is the row's
-// Hp query heads (padded to N >= 16), resident in smem for the row's tiles.
-// The contraction is L2-bandwidth bound (the whole key set stays L2-resident:
-// 32 MiB at 128K), so the kernel keeps STAGES gathers in flight.
+// The A operand is a gather of candidate key rows: four producer warps (one
+// thread per tile row) copy each row with 16-byte cp.async straight into the
+// 128-B-swizzled K-major layout the UMMA descriptor expects, LAG tiles in flight
+// per thread (cp.async.wait_group), then fence the generic->async proxy and
+// arrive on the stage's mbarrier.  B is the row's Hp query heads (padded to
+// N >= 16), resident in smem for the row's tiles.  The contraction is
+// L2-bandwidth bound (the whole key set stays L2-resident: 32 MiB at 128K).
+//
+// Warps: 0-3 producers, 4-7 epilogue (TMEM lane quadrants 0-3), 8 MMA issuer.
 #include "common.cuh"
 #include "ptx.cuh"
 
 namespace misa {
 
 struct RefineArgs {
+  const __nv_bfloat16* __restrict__ keys;  // [n_keys][D]
   const __nv_bfloat16* __restrict__ q;
   const float* __restrict__ w;
   const int32_t* __restrict__ cand;
@@ -26,13 +30,16 @@ struct RefineArgs {
   int64_t out_ld;
 };
 
-__device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t col,
-                                            int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(ptx::smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(ptx::smem_u32(bar))
-      : "memory");
+// 16-byte async global->shared copy; src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ptx::smem_u32(smem_dst)), "l"(gsrc),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 template <int D, int N>
@@ -53,9 +60,11 @@ struct RefineCfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
 
+constexpr int kRefineThreads = 288;
+constexpr int kLag = 2;  // cp.async tile groups in flight per producer thread
+
 template <int D, int N>
-__global__ void __launch_bounds__(192, 1)
-    refine_kernel(const __grid_constant__ CUtensorMap tmap_k, const RefineArgs a) {
+__global__ void __launch_bounds__(kRefineThreads, 1) refine_kernel(const RefineArgs a) {
   using C = RefineCfg<D, N>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -74,9 +83,8 @@ __global__ void __launch_bounds__(192, 1)
   const int P = gridDim.x, bid = blockIdx.x;
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&tmap_k);
     for (int i = 0; i < STAGES; ++i) {
-      ptx::mbar_init(&full_a[i], 1);
+      ptx::mbar_init(&full_a[i], 128);
       ptx::mbar_init(&empty_a[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -86,7 +94,7 @@ __global__ void __launch_bounds__(192, 1)
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 8) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -94,11 +102,13 @@ __global__ void __launch_bounds__(192, 1)
 
   auto item_at = [&](int it) { return (it & 1) ? (it + 1) * P - 1 - bid : it * P + bid; };
 
-  if (warp == 0) {
-    // Producer warp: lane l gathers candidate rows 4l..4l+3 of each 128-row tile
-    // (one coalesced index load per lane, one tile::gather4 per lane and K atom).
+  if (warp < 4) {
+    // Producers: thread i copies candidate row i of every 128-row tile.
+    const int pt = threadIdx.x;  // 0..127
     int s = 0;
     uint32_t ph = 0;
+    int pend[kLag + 1];
+    int npend = 0;
     for (int it = 0;; ++it) {
       const int idx = item_at(it);
       if (idx >= a.n_items) break;
@@ -106,32 +116,33 @@ __global__ void __launch_bounds__(192, 1)
       const int nc = a.n_cand[t];
       const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
       const int nt = (nc + 127) / 128;
-      auto load_idx = [&](int j, int (&r)[4]) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int i = j * 128 + 4 * lane + e;
-          const int ki = i < nc ? cr[i] : 0;
-          r[e] = ki < 0 ? 0 : ki;
-        }
-      };
-      int rn[4];
-      if (nt > 0) load_idx(0, rn);
+      int ki_next = (pt < nc) ? cr[pt] : -1;
       for (int j = 0; j < nt; ++j) {
-        int r[4] = {rn[0], rn[1], rn[2], rn[3]};
-        if (j + 1 < nt) load_idx(j + 1, rn);  // next tile's indices in flight while this one issues
-        if (lane == 0) {
-          ptx::mbar_wait(&empty_a[s], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
-        }
-        __syncwarp();
+        const int ki = ki_next;
+        if (j + 1 < nt) ki_next = ((j + 1) * 128 + pt < nc) ? cr[(j + 1) * 128 + pt] : -1;
+        ptx::mbar_wait(&empty_a[s], ph ^ 1);
+        uint8_t* dst = sA + s * C::A_BYTES;
+        const __nv_bfloat16* src = a.keys + (int64_t)(ki < 0 ? 0 : ki) * D;
+        const uint32_t nb = ki < 0 ? 0u : 16u;
 #pragma unroll
-        for (int at = 0; at < D / 64; ++at)
-          tma_gather4(sA + s * C::A_BYTES + at * C::A_ATOM + lane * 512, &tmap_k, &full_a[s], at * 64, r[0], r[1],
-                      r[2], r[3]);
+        for (int ch = 0; ch < D / 8; ++ch) cp_async16(dst + ptx::sw128_offset(pt, ch * 8, C::A_ATOM), src + ch * 8, nb);
+        cp_async_commit();
+        pend[npend++] = s;
+        if (npend > kLag) {
+          cp_async_wait<kLag>();
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&full_a[pend[0]]);
+#pragma unroll
+          for (int u = 0; u < kLag; ++u) pend[u] = pend[u + 1];
+          --npend;
+        }
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 1) {
+    cp_async_wait<0>();
+    ptx::fence_proxy_async_smem();
+    for (int u = 0; u < npend; ++u) ptx::mbar_arrive(&full_a[pend[u]]);
+  } else if (warp == 8) {
     if (ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
       int s = 0, acc = 0;
@@ -147,6 +158,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < nt; ++j) {
           ptx::mbar_wait(&tempty[acc], aph ^ 1);
           ptx::mbar_wait(&full_a[s], ph);
+          ptx::fence_proxy_async_smem();
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
           const uint32_t d_tmem = tmem_base + acc * N;
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    const int et = threadIdx.x - 64;
+    const int et = threadIdx.x - 128;
     const int quad = warp & 3;
     int acc = 0;
     uint32_t aph = 0;
@@ -223,7 +235,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 8) {
     __syncwarp();
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
@@ -231,13 +243,13 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <int D, int N>
-static int launch_refine_t(const CUtensorMap& map, const RefineArgs& a, cudaStream_t st) {
+static int launch_refine_t(const RefineArgs& a, cudaStream_t st) {
   using C = RefineCfg<D, N>;
   auto kern = refine_kernel<D, N>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
   const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
   if (grid <= 0) return MISA_OK;
-  kern<<<grid, 192, C::SMEM_BYTES, st>>>(map, a);
+  kern<<<grid, kRefineThreads, C::SMEM_BYTES, st>>>(a);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }
@@ -255,10 +267,9 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
   MISA_REQUIRE(n_heads >= 1 && n_heads <= n_heads_pad && n_heads_pad <= 128, "bad head counts");
   MISA_REQUIRE(n_rows >= 1 && n_keys >= 1, "empty input");
   if (n_items == 0) return MISA_OK;
-  CUtensorMap map;
-  int rc = make_tmap_bf16_gather(&map, keys, head_dim, n_keys);
-  if (rc) return rc;
+  MISA_REQUIRE((reinterpret_cast<uintptr_t>(keys) & 15) == 0, "keys must be 16-byte aligned");
   RefineArgs a{};
+  a.keys = static_cast<const __nv_bfloat16*>(keys);
   a.q = static_cast<const __nv_bfloat16*>(queries);
   a.w = weights;
   a.cand = cand;
@@ -274,7 +285,7 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
   cudaStream_t st = as_stream(stream);
   const int N = n_heads_pad < 16 ? 16 : n_heads_pad;
 #define MISA_REFINE_CASE(DD, NN) \
-  if (head_dim == DD && N == NN) return launch_refine_t<DD, NN>(map, a, st);
+  if (head_dim == DD && N == NN) return launch_refine_t<DD, NN>(a, st);
   MISA_REFINE_CASE(128, 16)
   MISA_REFINE_CASE(128, 32)
   MISA_REFINE_CASE(128, 64)

@@ -34,12 +34,36 @@ template <int NT>
 struct SelSh {
   static constexpr int NW = NT / 32;
   int cnt[2][NW];
+  int cnt3[2][3][NW];
   uint32_t red[NW];
   int tab[NT];  // per-(round, warp) selected counts, scanned in place
+  uint32_t bal[32 * (NT / 32)];  // v3: selection ballot of (round, warp)
+  int base[32 * (NT / 32)];      // v3: global rank of the first element of (round, warp)
   int wtot[NW];
   int lst_off[kMaxLists + 1];
   int lst_sel[kMaxLists + 1];
+  uint32_t bkey[256];  // boundary bucket (exact cut) staging
+  int32_t bidx[256];
+  int bcount;
+  uint32_t res_v;
+  int res_thr;
 };
+
+constexpr int kBucketMax = 256;
+
+// Warp-level: largest v with count(x >= v) >= j among this warp's values (x == 0: empty),
+// searching bits [hi, 0] on top of `prefix`.
+__device__ __forceinline__ uint32_t warp_kth(const uint32_t (&x)[8], int j, uint32_t prefix, int hi) {
+  uint32_t v = prefix;
+  for (int b = hi; b >= 0; --b) {
+    const uint32_t cand = v | (1u << b);
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c += x[i] >= cand;
+    if (__reduce_add_sync(0xffffffffu, c) >= j) v = cand;
+  }
+  return v;
+}
 
 template <int NT>
 __device__ __forceinline__ uint32_t block_reduce_or(uint32_t v, SelSh<NT>& sh) {
@@ -68,6 +92,37 @@ __device__ __forceinline__ int block_count(Pred pred, SelSh<NT>& sh, int& parity
   for (int i = 0; i < SelSh<NT>::NW; ++i) tot += sh.cnt[parity][i];
   parity ^= 1;
   return tot;
+}
+
+// Three block-wide counts (val >= c0, >= c1, >= c2) behind a single barrier.
+template <int NT, int EPT, typename Val>
+__device__ __forceinline__ void block_count3(Val val, uint32_t c0, uint32_t c1, uint32_t c2, SelSh<NT>& sh,
+                                             int& parity, int (&out)[3]) {
+  int n0 = 0, n1 = 0, n2 = 0;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const uint32_t x = val(r);
+    n0 += x >= c0;
+    n1 += x >= c1;
+    n2 += x >= c2;
+  }
+  n0 = __reduce_add_sync(0xffffffffu, n0);
+  n1 = __reduce_add_sync(0xffffffffu, n1);
+  n2 = __reduce_add_sync(0xffffffffu, n2);
+  if ((threadIdx.x & 31) == 0) {
+    sh.cnt3[parity][0][threadIdx.x >> 5] = n0;
+    sh.cnt3[parity][1][threadIdx.x >> 5] = n1;
+    sh.cnt3[parity][2][threadIdx.x >> 5] = n2;
+  }
+  __syncthreads();
+  out[0] = out[1] = out[2] = 0;
+#pragma unroll
+  for (int i = 0; i < SelSh<NT>::NW; ++i) {
+    out[0] += sh.cnt3[parity][0][i];
+    out[1] += sh.cnt3[parity][1][i];
+    out[2] += sh.cnt3[parity][2][i];
+  }
+  parity ^= 1;
 }
 
 // Largest v such that count(val(r) >= v) >= j, over valid slots; val() >= 1 for valid.
@@ -100,7 +155,24 @@ __device__ uint32_t kth_largest(Val val, int j, SelSh<NT>& sh, int& parity, int*
     const int hi = 31 - __clz(diff);
     v = (hi == 31) ? 0u : (first & ~((2u << hi) - 1u));
     cge = -1;
-    for (int b = hi; b >= min_bit; --b) {
+    // two bits per barrier: candidates v|11, v|10, v|01 of the next bit pair
+    int b = hi;
+    for (; b - 1 >= min_bit && min_bit == 0; b -= 2) {
+      const uint32_t hb = 1u << b, lb = 1u << (b - 1);
+      int c[3];
+      block_count3<NT, EPT>(val, v | hb | lb, v | hb, v | lb, sh, parity, c);
+      if (c[0] >= j) {
+        v |= hb | lb;
+        cge = c[0];
+      } else if (c[1] >= j) {
+        v |= hb;
+        cge = c[1];
+      } else if (c[2] >= j) {
+        v |= lb;
+        cge = c[2];
+      }
+    }
+    for (; b >= min_bit; --b) {
       const uint32_t cand = v | (1u << b);
       const int c = block_count<NT, EPT>([&](int r) { return val(r) >= cand; }, sh, parity);
       if (c >= j) {
@@ -136,10 +208,12 @@ __device__ __forceinline__ int merge_path(const int32_t* A, int na, const int32_
 // All NT threads merge A and B into D (each thread one contiguous output chunk).
 template <int NT>
 __device__ __forceinline__ void merge_pair(const int32_t* A, const float* As, int na, const int32_t* B,
-                                           const float* Bs, int nb, int32_t* D, float* Ds) {
+                                           const float* Bs, int nb, int32_t* D, float* Ds, int t = -1,
+                                           int nthr = NT) {
+  if (t < 0) t = threadIdx.x;
   const int M = na + nb;
-  const int chunk = (M + NT - 1) / NT;
-  const int d0 = min(M, (int)threadIdx.x * chunk), d1 = min(M, d0 + chunk);
+  const int chunk = (M + nthr - 1) / nthr;
+  const int d0 = min(M, t * chunk), d1 = min(M, d0 + chunk);
   if (d0 >= d1) return;
   int i = merge_path(A, na, B, nb, d0), j = d0 - i;
   for (int d = d0; d < d1; ++d) {
@@ -170,87 +244,229 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int x) {
   return lo;
 }
 
-// Core: key[EPT]/idx[EPT] in registers (element e = r*NT + tid, key 0 = empty slot),
-// NL lists with element offsets sh.lst_off[0..NL].  Selects the kk best
-// (key desc, idx asc) and writes them ascending by index to out[0..kk), scores
-// to outs (optional), -1 padding to k_out.  cidx/csc: smem scratch of kk entries.
+// ---------------------------------------------------------------- tau ----
 template <int NT, int EPT>
-__device__ void select_ordered(const uint32_t (&key)[EPT], const int32_t (&idx)[EPT], int N, int NL, int kk,
-                               SelSh<NT>& sh, int32_t* cidx, float* csc, int32_t* out, float* outs, int k_out) {
+__global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__ s, int64_t ld,
+                                                       const int32_t* __restrict__ prefix_len, int stride, int k,
+                                                       float beta, int64_t append_all, float* __restrict__ tau) {
+  __shared__ SelSh<NT> sh;
+  const int t = blockIdx.x;
+  const int n = prefix_len[t];
+  if (n <= append_all || n <= k) {
+    if (threadIdx.x == 0) tau[t] = -INFINITY;
+    return;
+  }
+  const int m = (n + stride - 1) / stride;
+  long long jj = (long long)ceilf(beta * (float)k * (float)m / (float)n);
+  jj = jj < 1 ? 1 : (jj > m ? m : jj);
+  const float* row = s + (int64_t)t * ld;
+  uint32_t key[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int e = r * NT + threadIdx.x;
+    key[r] = e < m ? float_key(row[e]) : 0u;
+  }
+  int parity = 0, cge, cgt;
+  // tau only has to be a lower bound of the j-th sampled score: resolve the sign, all 8
+  // exponent bits and 7 mantissa bits (key bits 31..16), round the rest down — at most
+  // 2^-7 relative below the exact value (a few more candidates, never fewer)
+  const uint32_t v =
+      kth_largest<NT, EPT>([&](int r) { return key[r]; }, (int)jj, sh, parity, &cge, &cgt, /*min_bit=*/16);
+  if (threadIdx.x == 0) tau[t] = key_float(v);
+}
+
+// ---------------------------------------------- v3 row selector core ----
+// Warp w owns the contiguous element range [w*WE, (w+1)*WE) of the row's
+// concatenated lists (WE = 32*EPT); lane l's slot r is element w*WE + 32r + l.
+// Keys live in registers (0 = empty slot), token indices in smem (sidx), so a
+// CTA needs few registers and several rows run per SM.
+template <int NT, int EPT>
+__device__ __forceinline__ int v3_elem(int r) {
+  return (threadIdx.x >> 5) * (EPT * 32) + r * 32 + (threadIdx.x & 31);
+}
+
+template <int NT, int EPT>
+__device__ void v3_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N, int kk, SelSh<NT>& sh, int& parity,
+                       uint32_t& v_out, int& thr_out) {
+  uint32_t lo_or = 0, a_and = 0xffffffffu;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    lo_or |= key[r];
+    if (key[r]) a_and &= key[r];
+  }
+  const uint32_t any_or = block_reduce_or<NT>(lo_or, sh);
+  const uint32_t all_and = ~block_reduce_or<NT>(~a_and, sh);
+  const uint32_t diff = any_or ^ all_and;
+  uint32_t v;
+  int b, above = 0, cge = N;
+  auto val = [&](int r) { return key[r]; };
+  if (diff == 0) {
+    v = all_and;
+    b = -1;
+  } else {
+    b = 31 - __clz(diff);
+    v = (b == 31) ? 0u : (all_and & ~((2u << b) - 1u));
+    while (b >= 1 && cge - above > kBucketMax) {
+      const uint32_t hb = 1u << b, lb = 1u << (b - 1);
+      int c[3];
+      block_count3<NT, EPT>(val, v | hb | lb, v | hb, v | lb, sh, parity, c);
+      if (c[0] >= kk) {
+        v |= hb | lb;
+        cge = c[0];
+      } else if (c[1] >= kk) {
+        above = c[0];
+        v |= hb;
+        cge = c[1];
+      } else if (c[2] >= kk) {
+        above = c[1];
+        v |= lb;
+        cge = c[2];
+      } else {
+        above = c[2];
+      }
+      b -= 2;
+    }
+    if (b == 0 && cge - above > kBucketMax) {
+      const int c = block_count<NT, EPT>([&](int r) { return key[r] >= (v | 1u); }, sh, parity);
+      if (c >= kk) {
+        v |= 1u;
+        cge = c;
+      } else {
+        above = c;
+      }
+      b = -1;
+    }
+  }
+  const int need = kk - above;
+  const int bucket = cge - above;
+  const uint32_t bmask = (b + 1 >= 32) ? 0u : ~((b >= 0) ? ((2u << b) - 1u) : 0u);
+  if (bucket <= kBucketMax) {
+    if (threadIdx.x == 0) sh.bcount = 0;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      if (key[r] != 0u && (key[r] & bmask) == (v & bmask)) {
+        const int p = atomicAdd(&sh.bcount, 1);
+        sh.bkey[p] = key[r];
+        sh.bidx[p] = sidx[v3_elem<NT, EPT>(r)];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      uint32_t x[8];
+      int32_t xi[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = lane + 32 * i;
+        x[i] = e < bucket ? sh.bkey[e] : 0u;
+        xi[i] = e < bucket ? sh.bidx[e] : 0x7fffffff;
+      }
+      const uint32_t vk = warp_kth(x, need, v & bmask, b);
+      int gt = 0, eq = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        gt += x[i] > vk;
+        eq += x[i] == vk;
+      }
+      gt = __reduce_add_sync(0xffffffffu, gt);
+      eq = __reduce_add_sync(0xffffffffu, eq);
+      const int need2 = need - gt;
+      int t = 0x7fffffff;
+      if (need2 < eq) {
+        uint32_t y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = x[i] == vk ? ~static_cast<uint32_t>(xi[i]) : 0u;
+        t = static_cast<int>(~warp_kth(y, need2, 0u, 31));
+      }
+      if (lane == 0) {
+        sh.res_v = vk;
+        sh.res_thr = t;
+      }
+    }
+    __syncthreads();
+    v_out = sh.res_v;
+    thr_out = sh.res_thr;
+    __syncthreads();
+    return;
+  }
+  // unsplittable bucket (all keys == v): keep the `need` smallest indices
+  int c2, c3;
+  const uint32_t t2 = kth_largest<NT, EPT>(
+      [&](int r) { return (key[r] == v) ? ~static_cast<uint32_t>(sidx[v3_elem<NT, EPT>(r)]) : 0u; }, need, sh,
+      parity, &c2, &c3);
+  v_out = v;
+  thr_out = (need < bucket) ? static_cast<int>(~t2) : 0x7fffffff;
+}
+
+// Select the kk best of the N staged elements (NL lists, each ascending by index,
+// offsets in sh.lst_off) and write them ascending to out[0..kk) (+ scores), -1 pad.
+template <int NT, int EPT>
+__device__ void v3_select(const uint32_t (&key)[EPT], const int32_t* sidx, int N, int NL, int kk, SelSh<NT>& sh,
+                          int32_t* cidx, float* csc, int32_t* out, float* outs, int k_out) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   int parity = 0;
   uint32_t v = 0;
   int thr = 0x7fffffff;
-  if (kk < N) {
-    int cge, cgt;
-    v = kth_largest<NT, EPT>([&](int r) { return key[r]; }, kk, sh, parity, &cge, &cgt);
-    const int need = kk - cgt;    // ties to keep
-    const int ties = cge - cgt;   // keys == v
-    if (need < ties) {
-      // keep the `need` smallest indices among the ties: (ties-need+1)-th largest of ~idx
-      int c2, c3;
-      const uint32_t t2 = kth_largest<NT, EPT>(
-          [&](int r) { return (key[r] == v) ? ~static_cast<uint32_t>(idx[r]) : 0u; }, need, sh, parity, &c2, &c3);
-      thr = static_cast<int>(~t2);
-    }
-  }
-  // ordered compaction: ballots per (round, warp) -> block scan -> ranks
-  auto selected = [&](int r) -> bool {
-    return key[r] != 0u && (kk >= N || key[r] > v || (key[r] == v && idx[r] <= thr));
-  };
+  if (kk < N) v3_cut<NT, EPT>(key, sidx, N, kk, sh, parity, v, thr);
+  uint32_t selm = 0;
+  int cnt = 0;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const uint32_t b = __ballot_sync(0xffffffffu, selected(r));
-    if (lane == 0) sh.tab[r * NW + w] = __popc(b);
+    bool sel = key[r] != 0u;
+    if (sel && kk < N) sel = key[r] > v || (key[r] == v && sidx[v3_elem<NT, EPT>(r)] <= thr);
+    selm |= (sel ? 1u : 0u) << r;
+    cnt += __popc(__ballot_sync(0xffffffffu, sel));
   }
+  if (lane == 0) sh.wtot[w] = cnt;
   __syncthreads();
-  {
-    // exclusive scan of the EPT*NW (<= NT) counts
-    constexpr int TS = EPT * NW;
-    const int x = tid < TS ? sh.tab[tid] : 0;
-    int inc = x;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += y;
-    }
-    if (lane == 31) sh.wtot[w] = inc;
-    __syncthreads();
-    int pre = 0;
-    for (int i = 0; i < w; ++i) pre += sh.wtot[i];
-    if (tid < TS) sh.tab[tid] = pre + inc - x;
-    __syncthreads();
-  }
+  int run = 0;
+  for (int i = 0; i < w; ++i) run += sh.wtot[i];
   const uint32_t lt = ptx::lanemask_lt();
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const int e = r * NT + tid;
-    const bool sel = selected(r);
-    const uint32_t b = __ballot_sync(0xffffffffu, sel);
-    const int rank = sh.tab[r * NW + w] + __popc(b & lt);
-    for (int l = 0; l <= NL; ++l)
-      if (sh.lst_off[l] == e && e < N) sh.lst_sel[l] = rank;
+    const bool sel = (selm >> r) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0) {
+      sh.bal[r * NW + w] = bal;
+      sh.base[r * NW + w] = run;
+    }
     if (sel) {
-      cidx[rank] = idx[r];
+      const int rank = run + __popc(bal & lt);
+      cidx[rank] = sidx[v3_elem<NT, EPT>(r)];
       if (csc) csc[rank] = key_float(key[r]);
     }
+    run += __popc(bal);
   }
-  if (tid == 0)
-    for (int l = 0; l <= NL; ++l)
-      if (sh.lst_off[l] >= N) sh.lst_sel[l] = kk;
   __syncthreads();
-  // pairwise merge-path rounds over the NL sorted runs; the last round writes `out`
+  // compacted-list boundaries: rank of each list's first element (from the stored ballots)
+  if (tid <= NL) {
+    const int e = sh.lst_off[tid];
+    int rk = kk;
+    if (e < N) {
+      const int ww = e / (EPT * 32), rr = (e % (EPT * 32)) / 32, ll = e % 32;
+      rk = sh.base[rr * NW + ww] + __popc(sh.bal[rr * NW + ww] & ((1u << ll) - 1u));
+    }
+    sh.lst_sel[tid] = rk;
+  }
+  __syncthreads();
+  // pairwise merge-path rounds over the NL sorted runs (pairs of a round run concurrently
+  // on disjoint thread groups); the last round writes `out`
   int32_t* src = cidx;
   float* srcs = csc;
   int32_t* tmp = cidx + k_out;
   float* tmps = csc ? csc + k_out : nullptr;
   int runs = NL;
   while (runs > 2) {
-    for (int p = 0; p + 1 < runs; p += 2) {
+    {
+      const int npairs = runs / 2;
+      const int per = NT / npairs;
+      const int p = min(tid / per, npairs - 1) * 2;
       const int a0 = sh.lst_sel[p], a1 = sh.lst_sel[p + 1], b1 = sh.lst_sel[p + 2];
-      merge_pair<NT>(src + a0, srcs ? srcs + a0 : nullptr, a1 - a0, src + a1, srcs ? srcs + a1 : nullptr, b1 - a1,
-                     tmp + a0, tmps ? tmps + a0 : nullptr);
+      if (tid / per < npairs)
+        merge_pair<NT>(src + a0, srcs ? srcs + a0 : nullptr, a1 - a0, src + a1, srcs ? srcs + a1 : nullptr,
+                       b1 - a1, tmp + a0, tmps ? tmps + a0 : nullptr, tid % per, per);
     }
     if (runs & 1) {
       for (int i = sh.lst_sel[runs - 1] + tid; i < sh.lst_sel[runs]; i += NT) {
@@ -289,40 +505,19 @@ __device__ void select_ordered(const uint32_t (&key)[EPT], const int32_t (&idx)[
   }
 }
 
-// ---------------------------------------------------------------- tau ----
-template <int NT, int EPT>
-__global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__ s, int64_t ld,
-                                                       const int32_t* __restrict__ prefix_len, int stride, int k,
-                                                       float beta, int64_t append_all, float* __restrict__ tau) {
-  __shared__ SelSh<NT> sh;
-  const int t = blockIdx.x;
-  const int n = prefix_len[t];
-  if (n <= append_all || n <= k) {
-    if (threadIdx.x == 0) tau[t] = -INFINITY;
-    return;
-  }
-  const int m = (n + stride - 1) / stride;
-  long long jj = (long long)ceilf(beta * (float)k * (float)m / (float)n);
-  jj = jj < 1 ? 1 : (jj > m ? m : jj);
-  const float* row = s + (int64_t)t * ld;
+// Run the row with the smallest register footprint that holds N elements.
+template <int NT, int EPT, typename LoadFn>
+__device__ void v3_dispatch(int N, LoadFn load, int NL, int kk, SelSh<NT>& sh, int32_t* sidx, int32_t* cidx,
+                            float* csc, int32_t* out, float* outs, int k_out) {
   uint32_t key[EPT];
-#pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int e = r * NT + threadIdx.x;
-    key[r] = e < m ? float_key(row[e]) : 0u;
-  }
-  int parity = 0, cge, cgt;
-  // tau only has to be a lower bound of the j-th sampled score: resolve the sign, all 8
-  // exponent bits and 10 mantissa bits (key bits 31..13), round the rest down — at most
-  // 2^-10 relative below the exact value (a few more candidates, never fewer)
-  const uint32_t v =
-      kth_largest<NT, EPT>([&](int r) { return key[r]; }, (int)jj, sh, parity, &cge, &cgt, /*min_bit=*/13);
-  if (threadIdx.x == 0) tau[t] = key_float(v);
+  load(key, sidx);
+  __syncthreads();
+  v3_select<NT, EPT>(key, sidx, N, NL, kk, sh, cidx, csc, out, outs, k_out);
 }
 
 // -------------------------------------------------- candidates -> top-k ----
 template <int NT, int EPT>
-__global__ void __launch_bounds__(NT) topk_kernel(const uint64_t* __restrict__ cand,
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) topk_kernel(const uint64_t* __restrict__ cand,
                                                   const int32_t* __restrict__ cand_count, int cap,
                                                   const int32_t* __restrict__ prefix_len, int k,
                                                   int32_t* __restrict__ topk, int64_t topk_ld,
@@ -341,14 +536,14 @@ __global__ void __launch_bounds__(NT) topk_kernel(const uint64_t* __restrict__ c
     if (threadIdx.x == 0 && flags) flags[t] = 0;
     return;
   }
-  int cnt[kQuadrants], off[kQuadrants + 1];
+  int off[kQuadrants + 1];
   bool overflow = false;
   off[0] = 0;
 #pragma unroll
   for (int q = 0; q < kQuadrants; ++q) {
-    cnt[q] = cand_count[(int64_t)t * kQuadrants + q];
-    overflow |= cnt[q] > cap;
-    off[q + 1] = off[q] + (cnt[q] < cap ? cnt[q] : cap);
+    const int c = cand_count[(int64_t)t * kQuadrants + q];
+    overflow |= c > cap;
+    off[q + 1] = off[q] + (c < cap ? c : cap);
   }
   const int total = off[kQuadrants];
   if (overflow || total < k || total > NT * EPT) {
@@ -358,37 +553,31 @@ __global__ void __launch_bounds__(NT) topk_kernel(const uint64_t* __restrict__ c
     return;
   }
   if (threadIdx.x <= kQuadrants) sh.lst_off[threadIdx.x] = off[threadIdx.x];
-  uint32_t key[EPT];
-  int32_t idx[EPT];
-  // all loads of a thread in flight before any use (candidate = key << 32 | score bits)
+  int32_t* sidx = reinterpret_cast<int32_t*>(dsm);
+  int32_t* cidx = sidx + NT * EPT;
+  float* csc = reinterpret_cast<float*>(cidx + 2 * k);
+  const uint64_t* rowc = cand + (int64_t)t * kQuadrants * cap;
+  auto load = [&](auto& key, int32_t* si) {
+    constexpr int E = sizeof(key) / sizeof(key[0]);
 #pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int e = r * NT + threadIdx.x;
-    uint2 rw = make_uint2(0u, 0u);
-    if (e < total) {
-      int q = 0;
-#pragma unroll
-      for (int qq = 1; qq < kQuadrants; ++qq) q += e >= off[qq];
-      rw = *reinterpret_cast<const uint2*>(cand + ((int64_t)t * kQuadrants + q) * cap + (e - off[q]));
+    for (int r = 0; r < E; ++r) {
+      const int e = v3_elem<NT, E>(r);
+      uint2 rw = make_uint2(0u, 0u);
+      if (e < total) {
+        const int q = (e >= off[1]) + (e >= off[2]) + (e >= off[3]);
+        rw = *reinterpret_cast<const uint2*>(rowc + (int64_t)q * cap + (e - off[q]));
+        si[e] = static_cast<int32_t>(rw.y);
+      }
+      key[r] = e < total ? float_key(__uint_as_float(rw.x)) : 0u;
     }
-    key[r] = rw.x;
-    idx[r] = static_cast<int32_t>(rw.y);
-  }
-#pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int e = r * NT + threadIdx.x;
-    key[r] = e < total ? float_key(__uint_as_float(key[r])) : 0u;
-  }
-  __syncthreads();
-  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
-  float* csc = reinterpret_cast<float*>(dsm + (size_t)k * 8);
-  select_ordered<NT, EPT>(key, idx, total, kQuadrants, k, sh, cidx, outs ? csc : nullptr, out, outs, k);
+  };
+  v3_dispatch<NT, EPT>(total, load, kQuadrants, k, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
   if (threadIdx.x == 0 && flags) flags[t] = 0;
 }
 
 // ------------------------------------------------------- dense rows ----
 template <int NT, int EPT>
-__global__ void __launch_bounds__(NT) dense_reg_kernel(const float* __restrict__ s, int64_t ld,
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(const float* __restrict__ s, int64_t ld,
                                                        const int32_t* __restrict__ idx, int64_t idx_ld,
                                                        const int32_t* __restrict__ row_len,
                                                        const int32_t* __restrict__ rows, int k,
@@ -403,21 +592,6 @@ __global__ void __launch_bounds__(NT) dense_reg_kernel(const float* __restrict__
   int32_t* out = topk + (int64_t)rr * topk_ld;
   float* outs = topk_scores ? topk_scores + (int64_t)rr * topk_ld : nullptr;
   const int kk = n < k ? n : k;
-  uint32_t key[EPT];
-  int32_t ix[EPT];
-#pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int e = r * NT + threadIdx.x;
-    key[r] = e < n ? float_key(row[e]) : 0u;
-    ix[r] = e < n ? (irow ? irow[e] : e) : 0x7fffffff;
-  }
-  if (threadIdx.x == 0) {
-    sh.lst_off[0] = 0;
-    sh.lst_off[1] = n;
-  }
-  __syncthreads();
-  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
-  float* csc = reinterpret_cast<float*>(dsm + (size_t)k * 8);
   if (kk <= 0) {
     for (int i = threadIdx.x; i < k; i += NT) {
       out[i] = -1;
@@ -425,7 +599,23 @@ __global__ void __launch_bounds__(NT) dense_reg_kernel(const float* __restrict__
     }
     return;
   }
-  select_ordered<NT, EPT>(key, ix, n, 1, kk, sh, cidx, outs ? csc : nullptr, out, outs, k);
+  if (threadIdx.x == 0) {
+    sh.lst_off[0] = 0;
+    sh.lst_off[1] = n;
+  }
+  int32_t* sidx = reinterpret_cast<int32_t*>(dsm);
+  int32_t* cidx = sidx + NT * EPT;
+  float* csc = reinterpret_cast<float*>(cidx + 2 * k);
+  auto load = [&](auto& key, int32_t* si) {
+    constexpr int E = sizeof(key) / sizeof(key[0]);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int e = v3_elem<NT, E>(r);
+      key[r] = e < n ? float_key(row[e]) : 0u;
+      if (e < n) si[e] = irow ? irow[e] : e;
+    }
+  };
+  v3_dispatch<NT, EPT>(n, load, 1, kk, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
 }
 
 // Global path for rows longer than the register capacity (exact fallback): MSB radix
@@ -571,29 +761,30 @@ __global__ void __launch_bounds__(NT) merge_kernel(const float* __restrict__ ps,
   }
   __syncthreads();
   const int N = sh.lst_off[n_parts];
-  uint32_t key[EPT];
-  int32_t ix[EPT];
-#pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int e = r * NT + threadIdx.x;
-    key[r] = 0u;
-    ix[r] = 0x7fffffff;
-    if (e < N) {
-      int p = 0;
-      while (p + 1 < n_parts && e >= sh.lst_off[p + 1]) ++p;
-      const int64_t at = p * part_stride + (int64_t)t * k_in + (e - sh.lst_off[p]);
-      key[r] = float_key(ps[at]);
-      ix[r] = pi[at];
-    }
-  }
   int32_t* out = topk + (int64_t)t * topk_ld;
   const int kk = N < k ? N : k;
   if (kk <= 0) {
     for (int i = threadIdx.x; i < k; i += NT) out[i] = -1;
     return;
   }
-  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
-  select_ordered<NT, EPT>(key, ix, N, n_parts, kk, sh, cidx, nullptr, out, nullptr, k);
+  int32_t* sidx = reinterpret_cast<int32_t*>(dsm);
+  int32_t* cidx = sidx + NT * EPT;
+  auto load = [&](auto& key, int32_t* si) {
+    constexpr int E = sizeof(key) / sizeof(key[0]);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int e = v3_elem<NT, E>(r);
+      key[r] = 0u;
+      if (e < N) {
+        int p = 0;
+        while (p + 1 < n_parts && e >= sh.lst_off[p + 1]) ++p;
+        const int64_t at = p * part_stride + (int64_t)t * k_in + (e - sh.lst_off[p]);
+        key[r] = float_key(ps[at]);
+        si[e] = pi[at];
+      }
+    }
+  };
+  v3_dispatch<NT, EPT>(N, load, n_parts, kk, sh, sidx, cidx, nullptr, out, nullptr, k);
 }
 
 }  // namespace misa
@@ -626,7 +817,7 @@ template <int NT, int EPT>
 struct TopkL {
   static int go(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl, int64_t T,
                 int k, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
-    const size_t bytes = (size_t)k * 16;
+    const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 16;
     MISA_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     topk_kernel<NT, EPT><<<(unsigned)T, NT, bytes, st>>>(cand, cc, cap, pl, k, topk, ld, ts, flags);
     MISA_LAUNCH_CHECK();
@@ -639,7 +830,7 @@ struct DenseL {
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* idx, int64_t idx_ld,
                 const int32_t* row_len, const int32_t* rows, int64_t n_rows, int k, int32_t* topk, int64_t tld,
                 float* ts) {
-    const size_t bytes = (size_t)k * 16;
+    const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 16;
     MISA_CUDA_TRY(
         cudaFuncSetAttribute(dense_reg_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     dense_reg_kernel<NT, EPT><<<(unsigned)n_rows, NT, bytes, st>>>(s, ld, idx, idx_ld, row_len, rows, k, topk, tld, ts);
@@ -652,7 +843,7 @@ template <int NT, int EPT>
 struct MergeL {
   static int go(cudaStream_t st, const float* ps, const int32_t* pi, int n_parts, int64_t stride, int64_t T, int k_in,
                 int k, int32_t* topk, int64_t ld) {
-    const size_t bytes = (size_t)k * 8;
+    const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 8;
     MISA_CUDA_TRY(cudaFuncSetAttribute(merge_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     merge_kernel<NT, EPT><<<(unsigned)T, NT, bytes, st>>>(ps, pi, n_parts, stride, k_in, k, topk, ld);
     MISA_LAUNCH_CHECK();
