@@ -28,6 +28,7 @@
  *   misa_select_dense     dsa.py:64-92       topk_tokens / topk_within over a dense score row
  *   misa_refine_scores    dsa.py:95-115      dsa_rescore (MISA-dagger fine stage), routing.py:144-174
  *   misa_merge_topk       (no reference counterpart: key-sharded multi-GPU merge)
+ *   misa_shard_map_indices (no reference counterpart: local -> global key index of a shard)
  */
 #ifndef MISA_B200_H_
 #define MISA_B200_H_
@@ -113,8 +114,10 @@ int misa_select_threshold(const float* sample_scores, int64_t ld, const int32_t*
                           int key_stride, int k, float beta, int64_t append_all_len, float* tau, void* stream);
 
 /* Exact top-k (score desc, index asc) from filtered candidates; output ascending indices.
- * Rows with n_t <= k select [0, n_t).  topk_scores (optional) holds the scores aligned
- * with topk.  flags[t] gets MISA_FLAG_* on overflow / underflow (row left -1). */
+ * Rows with n_t <= k select [0, n_t) (without scores; when topk_scores is requested such
+ * rows are selected from their candidates instead, which must then hold every key).
+ * topk_scores (optional) holds the scores aligned with topk.  flags[t] gets MISA_FLAG_*
+ * on overflow / underflow (row left -1). */
 int misa_select_topk(const uint64_t* cand, const int32_t* cand_count, int cap, const int32_t* prefix_len,
                      int64_t n_rows, int k, int32_t* topk, int64_t topk_ld, float* topk_scores, int32_t* flags,
                      void* stream);
@@ -136,6 +139,11 @@ int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const voi
  * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc). */
 int misa_merge_topk(const float* part_scores, const int32_t* part_idx, int n_parts, int64_t part_stride,
                     int64_t n_rows, int k_in, int k, int32_t* topk, int64_t topk_ld, void* stream);
+
+/* Block-cyclic key sharding: in place, local key index i of shard `shard` (of n_shards,
+ * blocks of `block` keys) -> global index ((i / block) * n_shards + shard) * block + i % block;
+ * -1 entries are kept. */
+int misa_shard_map_indices(int32_t* idx, int64_t n, int block, int n_shards, int shard, void* stream);
 
 #ifdef __cplusplus
 }

@@ -528,7 +528,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) topk_kernel(const uin
   const int n = prefix_len[t];
   int32_t* out = topk + (int64_t)t * topk_ld;
   float* outs = topk_scores ? topk_scores + (int64_t)t * topk_ld : nullptr;
-  if (n <= k) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73)
+  const int kk = n < k ? n : k;
+  if (n <= k && !outs) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73)
     for (int i = threadIdx.x; i < k; i += NT) {
       out[i] = i < n ? i : -1;
       if (outs && i >= n) outs[i] = -INFINITY;
@@ -546,7 +547,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) topk_kernel(const uin
     off[q + 1] = off[q] + (c < cap ? c : cap);
   }
   const int total = off[kQuadrants];
-  if (overflow || total < k || total > NT * EPT) {
+  if (overflow || total < kk || total > NT * EPT) {
     for (int i = threadIdx.x; i < k; i += NT) out[i] = -1;
     if (threadIdx.x == 0 && flags)
       flags[t] = (overflow || total > NT * EPT) ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
@@ -571,7 +572,14 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) topk_kernel(const uin
       key[r] = e < total ? float_key(__uint_as_float(rw.x)) : 0u;
     }
   };
-  v3_dispatch<NT, EPT>(total, load, kQuadrants, k, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
+  if (kk <= 0) {
+    for (int i = threadIdx.x; i < k; i += NT) {
+      out[i] = -1;
+      if (outs) outs[i] = -INFINITY;
+    }
+  } else {
+    v3_dispatch<NT, EPT>(total, load, kQuadrants, kk, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
+  }
   if (threadIdx.x == 0 && flags) flags[t] = 0;
 }
 
@@ -787,9 +795,26 @@ __global__ void __launch_bounds__(NT) merge_kernel(const float* __restrict__ ps,
   v3_dispatch<NT, EPT>(N, load, n_parts, kk, sh, sidx, cidx, nullptr, out, nullptr, k);
 }
 
+// Block-cyclic key shard: local key i of `rank` is global key ((i / bs) * G + rank) * bs + i % bs.
+__global__ void shard_map_kernel(int32_t* idx, int64_t n, int bs, int G, int rank) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = idx[i];
+  if (x >= 0) idx[i] = ((x / bs) * G + rank) * bs + x % bs;
+}
+
 }  // namespace misa
 
 using namespace misa;
+
+extern "C" int misa_shard_map_indices(int32_t* idx, int64_t n, int block, int n_shards, int shard, void* stream) {
+  MISA_REQUIRE(idx && n >= 0 && block >= 1 && n_shards >= 1 && shard >= 0 && shard < n_shards,
+               "bad shard map arguments");
+  if (n == 0) return MISA_OK;
+  shard_map_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(idx, n, block, n_shards, shard);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}
 
 namespace {
 // register-capacity configurations: (threads, elements per thread)

@@ -282,8 +282,11 @@ class IndexerEngine:
         return heads, hq, imp
 
     def select(self, x: PreparedInputs, heads: torch.Tensor | None, hq: int, k: int, out: torch.Tensor,
-               tag: str = "sel") -> int:
-        """Fused streaming top-k over the given head set (None = all heads). Returns #fallback rows."""
+               tag: str = "sel", scores: torch.Tensor | None = None) -> int:
+        """Fused streaming top-k over the given head set (None = all heads). Returns #fallback rows.
+
+        With ``scores`` (T, k) f32 the selected scores are returned too (aligned with ``out``)
+        and short rows are scored rather than short-cut — what a key shard's local top-k needs."""
         dev = x.keys.device
         stride, beta, cap = self.selector_params(k, x.L)
         append_all = 4 * cap
@@ -292,8 +295,9 @@ class IndexerEngine:
         ckey = x.causal_key or x.prefix_host.tobytes()
         s_items, s_tiles = self._dev_list(("samp", ckey, G, stride, append_all),
                                           lambda: self.group_items(x.prefix_host, G, stride, append_all), dev)
-        f_items, f_tiles = self._dev_list(("filt", ckey, G, k),
-                                          lambda: self.group_items(x.prefix_host, G, 1, k), dev)
+        min_len = 0 if scores is not None else k
+        f_items, f_tiles = self._dev_list(("filt", ckey, G, min_len),
+                                          lambda: self.group_items(x.prefix_host, G, 1, min_len), dev)
         Ls = (x.L + stride - 1) // stride
         tau = self._buf(tag + "_tau", (x.T,), torch.float32, dev)
         if s_items.numel():
@@ -317,17 +321,17 @@ class IndexerEngine:
         flags = self._buf(tag + "_flags", (x.T,), torch.int32, dev)
         self._mark(tag + ":select")
         _lib.call("misa_select_topk", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, _ptr(out), out.stride(0),
-                  None, _ptr(flags), stream)
+                  _ptr(scores), _ptr(flags), stream)
         self._mark(tag + ":end")
         if not self.check_overflow:
             return 0
         bad = torch.nonzero(flags).flatten()
         if bad.numel() == 0:
             return 0
-        self._dense_rows(x, heads, hq, k, out, bad.cpu().numpy())
+        self._dense_rows(x, heads, hq, k, out, bad.cpu().numpy(), scores)
         return int(bad.numel())
 
-    def _dense_rows(self, x: PreparedInputs, heads, hq, k, out, rows: np.ndarray):
+    def _dense_rows(self, x: PreparedInputs, heads, hq, k, out, rows: np.ndarray, scores=None):
         """Exact fallback: materialize full score rows for the flagged rows' groups, dense select."""
         dev = x.keys.device
         G = 256 // hq
@@ -343,7 +347,7 @@ class IndexerEngine:
                       x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles), 1, base, x.L, stream)
             sel = torch.from_numpy(rows[(rows // G) == g].astype(np.int32)).to(dev)
             _lib.call("misa_select_dense", base, x.L, None, 0, _ptr(x.prefix), _ptr(sel), sel.numel(), k, _ptr(out),
-                      out.stride(0), None, stream)
+                      out.stride(0), _ptr(scores), stream)
 
     def refine(self, x: PreparedInputs, cand: torch.Tensor, k: int, out: torch.Tensor):
         """K5 + dense select within candidates (MISA-dagger fine stage)."""

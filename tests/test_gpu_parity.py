@@ -285,3 +285,41 @@ def test_forced_fallback_rows_are_exact():
     assert eng.last_fallback_rows >= 5
     for t in range(L - 5, L):
         assert res.topk[t].tolist() == list(range(256))
+
+
+@pytest.mark.parametrize("method,G", [("dsa", 2), ("misa", 4), ("dsa", 8)])
+def test_virtual_key_shards_merge_to_single_gpu_result(method, G):
+    """Run every shard of a G-way key split on one GPU (local top-k with scores -> global
+    index map -> merge kernel) and compare with the unsharded engine, row for row."""
+    from paper_2605_07363_b200 import IndexerEngine, prepare_inputs, _lib
+    from paper_2605_07363_b200.engine import PreparedInputs
+    from paper_2605_07363_b200.sharded import KeyShardLayout, row_slices
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    L, H, k, B = 9000, 16, 512, 256
+    K = torch.randn(L, 64, device="cuda", generator=gen).bfloat16()
+    Q = torch.randn(L, H, 64, device="cuda", generator=gen).bfloat16()
+    W = torch.softmax(torch.randn(L, H, device="cuda", generator=gen), -1).float()
+    eng = IndexerEngine(method, budget_k=k, active_heads_h=4, block_size=B)
+    x = prepare_inputs(K, Q, W)
+    ref = eng.run_prepared(x).topk.clone()
+    heads = eng._ws["heads"].clone() if method == "misa" else None
+    hq = 8 if method == "misa" else x.Hp
+    per, T_pad = row_slices(L, G)
+    parts_i = torch.full((G, T_pad, k), -1, dtype=torch.int32, device="cuda")
+    parts_s = torch.full((G, T_pad, k), float("-inf"), device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for r in range(G):
+        lay = KeyShardLayout(G, r, B)
+        loc = torch.from_numpy(lay.local_keys(L)).cuda()
+        n_loc = lay.local_count(x.prefix_host)
+        Kl = x.keys.index_select(0, loc).contiguous()
+        xl = PreparedInputs(Kl, x.queries, x.weights, torch.from_numpy(n_loc.astype(np.int32)).cuda(), n_loc,
+                            Kl.shape[0], x.T, x.H, x.Hp, x.d, x.D, None)
+        e2 = IndexerEngine(method, budget_k=k, active_heads_h=4, block_size=B)
+        e2.select(xl, heads, hq, k, parts_i[r, :L], tag="shard", scores=parts_s[r, :L])
+        _lib.call("misa_shard_map_indices", parts_i[r].data_ptr(), parts_i[r].numel(), B, G, r, stream)
+    out = torch.empty((T_pad, k), dtype=torch.int32, device="cuda")
+    _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, T_pad * k, T_pad, k, k, out.data_ptr(), k,
+              stream)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:L], ref)

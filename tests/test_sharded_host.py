@@ -1,0 +1,102 @@
+"""Key-sharded (multi-GPU) host logic on CPU: shard layout math and the gloo world_size-2
+exchange + merge pipeline, with the oracle standing in for the per-rank local top-k."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import misa_oracle as O
+from paper_2605_07363_b200.sharded import KeyShardLayout, exchange_by_rows, row_slices
+
+
+@pytest.mark.parametrize("G,B,L", [(2, 16, 100), (4, 8, 257), (8, 1024, 20000), (3, 5, 1)])
+def test_layout_partitions_keys(G, B, L):
+    owned = [KeyShardLayout(G, r, B).local_keys(L) for r in range(G)]
+    allk = np.sort(np.concatenate(owned))
+    assert allk.tolist() == list(range(L))  # disjoint cover
+    for r in range(G):
+        lay = KeyShardLayout(G, r, B)
+        loc = owned[r]
+        assert np.all(np.diff(loc) > 0)
+        assert lay.to_global(np.arange(loc.shape[0])).tolist() == loc.tolist()  # monotone map
+        ns = np.arange(0, L + 1)
+        brute = np.searchsorted(loc, ns, side="left")  # local keys with global index < n
+        assert lay.local_count(ns).tolist() == brute.tolist()
+    # block-cyclic balance of causal work: per-rank sum of local prefix lengths
+    work = [KeyShardLayout(G, r, B).local_count(np.arange(1, L + 1)).sum() for r in range(G)]
+    if L >= 8 * G * B:
+        assert max(work) / max(1, min(work)) < 1.3
+
+
+def _merge_np(parts_i, parts_s, k):
+    """Reference merge: union of the per-rank lists, (score desc, index asc), ascending output."""
+    out = np.full((parts_i.shape[1], k), -1, np.int64)
+    for t in range(parts_i.shape[1]):
+        pairs = [(float(parts_s[p, t, j]), int(parts_i[p, t, j]))
+                 for p in range(parts_i.shape[0]) for j in range(parts_i.shape[2]) if parts_i[p, t, j] >= 0]
+        pairs.sort(key=lambda x: (-x[0], x[1]))
+        sel = sorted(i for _, i in pairs[:k])
+        out[t, : len(sel)] = sel
+    return out
+
+
+def _worker(rank, world, port, L, H, d, k, B, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        K, Q, W = O.synthetic_prefill(77, L, H, d)
+        lay = KeyShardLayout(world, rank, B)
+        loc = lay.local_keys(L)
+        n_loc = lay.local_count(np.arange(1, L + 1))
+        per, T_pad = row_slices(L, world)
+        li = np.full((T_pad, k), -1, np.int64)
+        ls = np.full((T_pad, k), -np.inf)
+        for t in range(L):
+            if n_loc[t] == 0:
+                continue
+            keys = K[loc[: n_loc[t]]]
+            sc = O.gated_relu_scores(keys, Q[t], W[t], "fast32")
+            sel = O.topk_tokens(sc, k)  # local indices, ascending
+            li[t, : sel.shape[0]] = lay.to_global(sel)
+            ls[t, : sel.shape[0]] = sc[sel]
+        pi, ps = exchange_by_rows(torch.from_numpy(li), torch.from_numpy(ls), world)
+        got = _merge_np(pi.numpy(), ps.numpy(), k)
+        ok = True
+        for j in range(per):
+            t = rank * per + j
+            if t >= L:
+                continue
+            ref = O.dsa_select(K[: t + 1], Q[t], W[t], k, "fast32")["selection"]
+            row = got[j][got[j] >= 0]
+            ok &= row.tolist() == ref.tolist()
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_sharded_exchange_and_merge_equal_dense(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    L, H, d, k, B = 300, 8, 16, 24, 16
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, L, H, d, k, B, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()), res
