@@ -37,7 +37,7 @@ def test_abi_library_exports_every_header_symbol():
 
 
 def test_sass_contains_tcgen05_and_tma():
-    """The shipped library carries tcgen05 MMAs, TMEM loads and TMA (incl. gather4) in SASS."""
+    """The shipped library carries tcgen05 MMAs, TMEM loads, TMA and cp.async gathers in SASS."""
     import shutil
     import subprocess
     from paper_2605_07363_b200 import _build
@@ -47,7 +47,7 @@ def test_sass_contains_tcgen05_and_tma():
     if not os.path.exists(tool):
         pytest.skip("cuobjdump not available")
     sass = subprocess.run([tool, "-sass", _build.LIB], capture_output=True, text=True).stdout
-    for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "GATHER4"):
+    for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "LDGSTS"):
         assert mnem in sass, mnem
     assert "HMMA" not in sass.replace("UTCHMMA", "")  # no legacy mma.sync path
 
