@@ -213,6 +213,10 @@ def run_ours(a):
         from paper_2605_07363_b200.sharded import ShardedIndexer
         eng_m = ShardedIndexer("misa", world=world, rank=rank, budget_k=a.k, active_heads_h=a.h, block_size=a.B)
         eng_d = ShardedIndexer("dsa", world=world, rank=rank, budget_k=a.k, block_size=a.B)
+
+    class _Out:
+        def __init__(self, topk):
+            self.topk = topk
     else:
         eng_m = IndexerEngine("misa", budget_k=a.k, active_heads_h=a.h, block_size=a.B)
         eng_d = IndexerEngine("dsa", budget_k=a.k)
@@ -249,7 +253,7 @@ def run_ours(a):
             stages[n0] = stages.get(n0, 0.0) + e0.elapsed_time(e1)
         eng_m.stage_events = None
     else:
-        res_m = step_m()
+        res_m = _Out(eng_m.run(K, Q, W, gather=True))
 
     # --- dense DSA on the same inputs (the comparison kernel)
     dsa_ms = max_over_ranks(_time_steps(step_d, a.steps, a.warmup, barrier))
@@ -263,7 +267,7 @@ def run_ours(a):
             dstages[n0] = dstages.get(n0, 0.0) + e0.elapsed_time(e1)
         eng_d.stage_events = None
     else:
-        res_d = step_d()
+        res_d = _Out(eng_d.run(K, Q, W, gather=True))
 
     hier_ms = None
     hstages = {}
@@ -349,7 +353,7 @@ def run_ours(a):
     layer_frac = flops_misa / (misa_ms * 1e-3) / 1e12 / tc_sust
 
     cpu = None
-    if not a.no_cpu:
+    if not a.no_cpu and world == 1:
         from oracle import cpu_bench
         cores = os.cpu_count() or 1
         srows = cpu_bench.sample_rows(L, T, max(16, 2 * cores))
