@@ -213,13 +213,13 @@ def run_ours(a):
         from paper_2605_07363_b200.sharded import ShardedIndexer
         eng_m = ShardedIndexer("misa", world=world, rank=rank, budget_k=a.k, active_heads_h=a.h, block_size=a.B)
         eng_d = ShardedIndexer("dsa", world=world, rank=rank, budget_k=a.k, block_size=a.B)
+    else:
+        eng_m = IndexerEngine("misa", budget_k=a.k, active_heads_h=a.h, block_size=a.B)
+        eng_d = IndexerEngine("dsa", budget_k=a.k)
 
     class _Out:
         def __init__(self, topk):
             self.topk = topk
-    else:
-        eng_m = IndexerEngine("misa", budget_k=a.k, active_heads_h=a.h, block_size=a.B)
-        eng_d = IndexerEngine("dsa", budget_k=a.k)
     x = prepare_inputs(K, Q, W) if world == 1 else None
 
     def step_m():
