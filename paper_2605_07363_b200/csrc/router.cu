@@ -37,16 +37,19 @@ struct RouteArgs {
 
 template <int D>
 struct RouteCfg {
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = 3;
   static constexpr int A_ATOM = 128 * 128;
   static constexpr int A_BYTES = A_ATOM * (D / 64);
   static constexpr int B_ATOM = 128 * 128;      // 128 pooled rows x 64 dims
   static constexpr int B_PLANE = B_ATOM * (D / 64);
   static constexpr int B_BYTES = 3 * B_PLANE;
+  static constexpr int P_ROWS = 16;             // query rows per tile (Hp >= 8)
+  static constexpr int P_BYTES = P_ROWS * D * 4;  // partial-block prefix rows of a tile
   static constexpr int NUM_THREADS = 192;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = STAGES * A_BYTES;
-  static constexpr int OFF_BAR = OFF_B + B_BYTES;
+  static constexpr int OFF_P = OFF_B + B_BYTES;
+  static constexpr int OFF_BAR = OFF_P + STAGES * P_BYTES;
   static constexpr int NUM_BARS = 2 * STAGES + 6;
   static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
@@ -65,6 +68,7 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem + C::OFF_A;
   uint8_t* sB = smem + C::OFF_B;
+  float* sP = reinterpret_cast<float*>(smem + C::OFF_P);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* full_a = bars;
   uint64_t* empty_a = bars + STAGES;
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(192, 1)
     ptx::tma_prefetch_desc(&tmap_p);
     for (int i = 0; i < STAGES; ++i) {
       ptx::mbar_init(&full_a[i], 1);
-      ptx::mbar_init(&empty_a[i], 1);
+      ptx::mbar_init(&empty_a[i], 1 + 128);  // MMA commit + the epilogue's q / prefix reads
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
@@ -106,8 +110,8 @@ __global__ void __launch_bounds__(192, 1)
         const int idx = route_item(it, P, bid);
         if (idx >= a.n_items) break;
         const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
-        if (ncols == 0) continue;
-        if (chunk != cur_chunk) {
+        if (ncols == 0 && chunk != 0) continue;
+        if (ncols > 0 && chunk != cur_chunk) {
           if (nb > 0) ptx::mbar_wait(bempty, (nb - 1) & 1);
           ptx::mbar_arrive_expect_tx(bfull, C::B_BYTES);
           for (int p = 0; p < 3; ++p)
@@ -117,10 +121,29 @@ __global__ void __launch_bounds__(192, 1)
           cur_chunk = chunk;
           ++nb;
         }
+        // chunk 0 also stages each row's partial-block prefix sum P[n-1] for the epilogue
+        const int rows = 128 >> a.hp_log2;
+        int np = 0;
+        if (chunk == 0)
+          for (int rr = 0; rr < rows; ++rr) {
+            const int t = a.it_tile[idx] * rows + rr;
+            if (t < a.T && a.prefix_len[t] % a.B) ++np;
+          }
         ptx::mbar_wait(&empty_a[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
+        ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES + np * D * 4);
         for (int at = 0; at < D / 64; ++at)
           ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_q, &full_a[s], at * 64, a.it_tile[idx] * 128);
+        if (np)
+          for (int rr = 0; rr < rows; ++rr) {
+            const int t = a.it_tile[idx] * rows + rr;
+            const int n = t < a.T ? a.prefix_len[t] : 0;
+            if (t < a.T && n % a.B)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      ptx::smem_u32(sP + (s * C::P_ROWS + rr) * D)),
+                  "l"(a.prefix + (int64_t)(n - 1) * D), "r"(D * 4), "r"(ptx::smem_u32(&full_a[s]))
+                  : "memory");
+          }
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
@@ -133,7 +156,13 @@ __global__ void __launch_bounds__(192, 1)
         const int idx = route_item(it, P, bid);
         if (idx >= a.n_items) break;
         const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
-        if (ncols == 0) continue;
+        if (ncols == 0 && chunk != 0) continue;
+        if (ncols == 0) {  // partial-block-only tile: no MMA, just hand the stage back
+          ptx::mbar_wait(&full_a[s], ph);
+          ptx::mbar_arrive(&empty_a[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+          continue;
+        }
         if (chunk != cur_chunk) {
           if (nb > 0) ptx::mma_commit(bempty);  // all MMAs on the previous chunk's planes
           ptx::mbar_wait(bfull, nb & 1);
@@ -164,13 +193,15 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int quad = warp & 3;
-    int acc = 0;
-    uint32_t aph = 0;
+    int acc = 0, s = 0;
+    uint32_t aph = 0, ph = 0;
     for (int it = 0;; ++it) {
       const int idx = route_item(it, P, bid);
       if (idx >= a.n_items) break;
       const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
-      const int64_t grow = (int64_t)a.it_tile[idx] * 128 + quad * 32 + lane;
+      if (ncols == 0 && chunk != 0) continue;
+      const int lrow = quad * 32 + lane;  // A tile row = (t, j) pair
+      const int64_t grow = (int64_t)a.it_tile[idx] * 128 + lrow;
       const int t = (int)(grow >> a.hp_log2);
       const int j = (int)(grow & (a.Hp - 1));
       const int n = t < a.T ? a.prefix_len[t] : 0;
@@ -184,7 +215,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int c = 0; c < ncols; c += 32) {  // ncols is uniform per item
           uint32_t r[32];
           ptx::tmem_ld_x32(taddr + c, r);
-          ptx::tmem_wait_ld();
+          ptx::tmem_wait_ld_dep(r);
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (c + i < lim) sum += fmaxf(__uint_as_float(r[i]), 0.f);
@@ -193,28 +224,29 @@ __global__ void __launch_bounds__(192, 1)
         ptx::mbar_arrive(&tempty[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
-      if (t < a.T) {
-        const int rem = n - nf * a.B;
-        if (chunk == 0 && rem > 0) {
-          // partial last block: mean over keys [nf*B, n) = P[n-1] / rem
-          const uint4* qv = reinterpret_cast<const uint4*>(a.q + grow * D);
-          const float4* pv = reinterpret_cast<const float4*>(a.prefix + (int64_t)(n - 1) * D);
-          float dot = 0.f;
+      // partial last block: mean over keys [nf*B, n) = P[n-1] / rem, with q from the A stage
+      ptx::mbar_wait(&full_a[s], ph);
+      const int rem = n - nf * a.B;
+      if (t < a.T && chunk == 0 && rem > 0) {
+        const uint8_t* qa = sA + s * C::A_BYTES;
+        const float4* pv = reinterpret_cast<const float4*>(sP + (s * C::P_ROWS + (lrow >> a.hp_log2)) * D);
+        float dot = 0.f;
 #pragma unroll 4
-          for (int c = 0; c < D / 8; ++c) {
-            const uint4 u = qv[c];
-            const float4 p0 = pv[2 * c], p1 = pv[2 * c + 1];
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-            float2 f;
-            f = __bfloat1622float2(h[0]); dot = fmaf(f.x, p0.x, dot); dot = fmaf(f.y, p0.y, dot);
-            f = __bfloat1622float2(h[1]); dot = fmaf(f.x, p0.z, dot); dot = fmaf(f.y, p0.w, dot);
-            f = __bfloat1622float2(h[2]); dot = fmaf(f.x, p1.x, dot); dot = fmaf(f.y, p1.y, dot);
-            f = __bfloat1622float2(h[3]); dot = fmaf(f.x, p1.z, dot); dot = fmaf(f.y, p1.w, dot);
-          }
-          sum += fmaxf(dot / (float)rem, 0.f);
+        for (int c = 0; c < D / 8; ++c) {
+          const uint4 u = *reinterpret_cast<const uint4*>(qa + ptx::sw128_offset(lrow, c * 8, C::A_ATOM));
+          const float4 p0 = pv[2 * c], p1 = pv[2 * c + 1];
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+          float2 f;
+          f = __bfloat1622float2(h[0]); dot = fmaf(f.x, p0.x, dot); dot = fmaf(f.y, p0.y, dot);
+          f = __bfloat1622float2(h[1]); dot = fmaf(f.x, p0.z, dot); dot = fmaf(f.y, p0.w, dot);
+          f = __bfloat1622float2(h[2]); dot = fmaf(f.x, p1.x, dot); dot = fmaf(f.y, p1.y, dot);
+          f = __bfloat1622float2(h[3]); dot = fmaf(f.x, p1.z, dot); dot = fmaf(f.y, p1.w, dot);
         }
-        a.partial[((int64_t)chunk * a.T + t) * a.Hp + j] = sum;
+        sum += fmaxf(dot / (float)rem, 0.f);
       }
+      ptx::mbar_arrive(&empty_a[s]);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+      if (t < a.T) a.partial[((int64_t)chunk * a.T + t) * a.Hp + j] = sum;
     }
   }
 
