@@ -16,6 +16,23 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Dynamic smem base rounded up to 1024 B (SW128 operand atoms) by pointer arithmetic
+// on the __shared__ array itself, so the compiler keeps the shared address space
+// and emits LDS/STS (an integer round-trip would demote every access to generic LD/ST).
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
+// Predicated 8-byte global store (no branch around it).
+__device__ __forceinline__ void st_global_u64_if(uint64_t* p, uint64_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "setp.ne.b32 P, %2, 0;\n\t"
+      "@P st.global.u64 [%0], %1;\n\t}" ::"l"(p),
+      "l"(v), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
@@ -164,6 +181,13 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
         "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_x32p(uint32_t taddr, uint32_t* r) {
+  tmem_ld_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+}
+__device__ __forceinline__ void tmem_wait_ld_dep32p(uint32_t* r) {
+  tmem_wait_ld_dep(*reinterpret_cast<uint32_t(*)[32]>(r));
 }
 
 __device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t* r) {

@@ -17,7 +17,8 @@
 //               TMEM lane quadrant w%4 and one column split): gather
 //               the item's query/head vectors into smem (the B operand, resident
 //               for the whole key scan), then per tile a software-pipelined
-//               tcgen05.ld drain -> ReLU * w * sum (packed FFMA2) -> either store
+//               tcgen05.ld of the warp's whole column slice, early release of the
+//               accumulator, ReLU * w * sum (packed FFMA2) -> either store
 //               the score row (MATERIALIZE) or append (score, key) >= tau to the
 //               row's per-quadrant candidate list (FILTER: the fused top-k's
 //               candidate pass; lists stay in ascending key order).
@@ -70,6 +71,16 @@ __device__ __forceinline__ void drain(uint32_t taddr, const float* __restrict__ 
   }
 }
 
+// Reduce a warp's whole register-resident column slice, chunk by chunk.
+template <int HQ, int QW, int NCH, int C>
+__device__ __forceinline__ void reduce_all(const uint32_t* r, const float* __restrict__ wcol, float (&sc)[QW],
+                                           float2& p0, float2& p1) {
+  if constexpr (C < NCH) {
+    reduce16<HQ, QW, C>(r + C * 16, wcol, sc, p0, p1);
+    reduce_all<HQ, QW, NCH, C + 1>(r, wcol, sc, p0, p1);
+  }
+}
+
 struct ScoreArgs {
   const __nv_bfloat16* __restrict__ q;  // [T][Hp][D]
   const float* __restrict__ w;          // [T][Hp]
@@ -108,8 +119,7 @@ struct ScoreCfg {
   static constexpr int OFF_W = OFF_B + B_BYTES;
   static constexpr int OFF_LIM = OFF_W + kTileCols * 4;
   static constexpr int OFF_TAU = OFF_LIM + 32 * 4;
-  static constexpr int OFF_STG = OFF_TAU + 32 * 4;  // FILTER append staging: [warp][QW][32] f32
-  static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * QW * 32 * 4;
+  static constexpr int OFF_BAR = OFF_TAU + 32 * 4;
   static constexpr int NUM_BARS = 2 * STAGES + 5;
   static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
@@ -130,13 +140,12 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
   using C = ScoreCfg<D, HQ>;
   constexpr int G = C::G, STAGES = C::STAGES, QW = C::QW, EPI_THREADS = C::EPI_THREADS;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* sA = smem + C::OFF_A;
   uint8_t* sB = smem + C::OFF_B;
   float* sW = reinterpret_cast<float*>(smem + C::OFF_W);
   int* sLim = reinterpret_cast<int*>(smem + C::OFF_LIM);
   float* sTau = reinterpret_cast<float*>(smem + C::OFF_TAU);
-  float* sStg = reinterpret_cast<float*>(smem + C::OFF_STG);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* full_a = bars;
   uint64_t* empty_a = bars + STAGES;
@@ -228,7 +237,6 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
     const int et = threadIdx.x - 64;
     const int quad = warp & 3;
     const int split = e >> 2;
-    float* stg = sStg + e * (QW * 32);
     int acc = 0;
     uint32_t aph = 0;
     for (int it = 0;; ++it) {
@@ -276,17 +284,19 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
       if (et == 0) ptx::mbar_arrive(bfull);
 
       const int qbase = split * QW;  // first query row (within the item) of this warp
-      int lim_r[QW];
-      float tau_r[QW];
+      int lim_min = 0x7fffffff;
 #pragma unroll
-      for (int q = 0; q < QW; ++q) {
-        lim_r[q] = sLim[qbase + q];
-        tau_r[q] = sTau[qbase + q];
-      }
+      for (int q = 0; q < QW; ++q) lim_min = min(lim_min, sLim[qbase + q]);
       const float* wcol = sW + split * C::COLS;
-      int cnt = 0;  // FILTER: lane q counts candidates of query qbase+q seen by this warp
-      uint64_t* dst = nullptr;
-      if (FILTER && lane < QW) dst = a.cand + ((int64_t)(row0 + qbase + lane) * kQuadrants + quad) * a.cap;
+      // FILTER: cnt[q] is the (warp-uniform) number of candidates of query qbase+q
+      // this warp has appended so far; lists stay in ascending key order.
+      int cnt[QW];
+#pragma unroll
+      for (int q = 0; q < QW; ++q) cnt[q] = 0;
+      const uint32_t lt = ptx::lanemask_lt();
+      uint64_t* dst0 = nullptr;
+      const int qstride = kQuadrants * a.cap;  // elements between consecutive rows' lists
+      if (FILTER) dst0 = a.cand + (static_cast<int64_t>(row0 + qbase) * kQuadrants + quad) * a.cap;
       for (int jt = 0; jt < nt; ++jt) {
         ptx::mbar_wait(&tfull[acc], aph);
         ptx::tc_fence_after();
@@ -296,52 +306,59 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
             tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols + split * C::COLS;
         float sc[QW];
         float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
-        uint32_t ra[16], rb[16];
-        ptx::tmem_ld_x16(taddr, ra);
-        ptx::tmem_wait_ld_dep16(ra);
-        drain<HQ, QW, C::NCH, 0>(taddr, wcol, sc, p0, p1, ra, rb);
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&tempty[acc]);
+        if constexpr (C::COLS <= 64) {
+          // whole column slice in registers at once: the accumulator buffer is handed
+          // back to the MMA warp before any arithmetic, so the tensor pipe never waits
+          // on the epilogue's latency, only on its throughput.
+          uint32_t r[C::COLS];
+#pragma unroll
+          for (int c = 0; c < C::COLS; c += 32) ptx::tmem_ld_x32p(taddr + c, r + c);
+#pragma unroll
+          for (int c = 0; c < C::COLS; c += 32) ptx::tmem_wait_ld_dep32p(r + c);
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty[acc]);
+          reduce_all<HQ, QW, C::NCH, 0>(r, wcol, sc, p0, p1);
+        } else {
+          uint32_t ra[16], rb[16];
+          ptx::tmem_ld_x16(taddr, ra);
+          ptx::tmem_wait_ld_dep16(ra);
+          drain<HQ, QW, C::NCH, 0>(taddr, wcol, sc, p0, p1, ra, rb);
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty[acc]);
+        }
         if (++acc == 2) { acc = 0; aph ^= 1; }
 
         if constexpr (FILTER) {
-          // vote-transposed append: every lane stages its QW scores, one ballot per
-          // query gives that query's passing-lane mask, and lane q appends query q's
-          // candidates in ascending key order (lists stay sorted by token index).
-          uint32_t mq = 0;
-          bool any = false;
+          // one ballot per query: passing lanes write at (count so far + rank among the
+          // warp's passing lanes), so no staging, no serial loop and no divergence.
+          // The prefix bound is only tested on the warp's last (diagonal) tile.
+          const bool edge = key0 + 31 >= lim_min;
+          const uint64_t khi = static_cast<uint64_t>(static_cast<uint32_t>(key)) << 32;
 #pragma unroll
           for (int q = 0; q < QW; ++q) {
-            const bool pass = key < lim_r[q] && sc[q] >= tau_r[q];
+            bool pass = sc[q] >= sTau[qbase + q];
+            if (edge) pass = pass && key < sLim[qbase + q];
             const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-            any |= bal != 0u;
-            if (lane == q) mq = bal;
-            stg[q * 32 + lane] = sc[q];
+            const int pos = cnt[q] + __popc(bal & lt);
+            ptx::st_global_u64_if(dst0 + static_cast<uint32_t>(q * qstride + pos), khi | __float_as_uint(sc[q]),
+                                  pass && pos < a.cap);
+            cnt[q] += __popc(bal);
           }
-          if (any) {
-            __syncwarp();
-            int pos = cnt;
-            cnt += __popc(mq);
-            while (mq) {
-              const int l = __ffs(mq) - 1;
-              mq &= mq - 1;
-              if (pos < a.cap)
-                dst[pos] = (static_cast<uint64_t>(static_cast<uint32_t>(key0 + l)) << 32) |
-                           __float_as_uint(stg[lane * 32 + l]);
-              ++pos;
-            }
-          }
-          __syncwarp();
         } else {
+          float* o = a.out + static_cast<int64_t>(row0 + qbase) * a.out_ld + key;
 #pragma unroll
           for (int q = 0; q < QW; ++q)
-            if (key < lim_r[q]) a.out[(int64_t)(row0 + qbase + q) * a.out_ld + key] = sc[q];
+            if (key < sLim[qbase + q]) o[q * a.out_ld] = sc[q];
         }
       }
       if constexpr (FILTER) {
+        int mine = 0;
+#pragma unroll
+        for (int q = 0; q < QW; ++q)
+          if (lane == q) mine = cnt[q];
         if (lane < QW) {
           const int row = row0 + qbase + lane;
-          if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = cnt;
+          if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = mine;
         }
       }
       ptx::named_bar_sync(1, EPI_THREADS);
