@@ -33,6 +33,19 @@ __device__ __forceinline__ void st_global_u64_if(uint64_t* p, uint64_t v, bool p
       : "memory");
 }
 
+// Predicated 8-byte global store of {lo, hi} (the u64 hi:lo) to base[idx], with the
+// address formed by one wide multiply-add (no 64-bit add chains, no packing).
+__device__ __forceinline__ void st_global_v2_idx_if(const void* base, uint32_t idx, uint32_t lo, uint32_t hi,
+                                                    bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t.reg .b64 A;\n\t"
+      "setp.ne.b32 P, %4, 0;\n\t"
+      "mad.wide.u32 A, %1, 8, %0;\n\t"
+      "@P st.global.v2.b32 [A], {%2, %3};\n\t}" ::"l"(base),
+      "r"(idx), "r"(lo), "r"(hi), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
@@ -190,6 +203,22 @@ __device__ __forceinline__ void tmem_wait_ld_dep32p(uint32_t* r) {
   tmem_wait_ld_dep(*reinterpret_cast<uint32_t(*)[32]>(r));
 }
 
+// 16 lanes x 256 bits, 8 repetitions along columns: thread t gets lanes (t/4, t/4+8)
+// at columns 8g + 2(t%4) + {0,1} in r[4g .. 4g+3] = (l0,c0) (l0,c1) (l8,c0) (l8,c1)
+// (layout probed on B200: tools/ubench_tmem_layout.cu).
+__device__ __forceinline__ void tmem_ld_16x256b_x8(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x8.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -258,5 +287,20 @@ __device__ __forceinline__ void gate_relu4(float2& s0, float2& s1, const float4 
 }
 __device__ __forceinline__ float gate_relu_finish(const float2 s0, const float2 s1) {
   return (s0.x + s0.y) + (s1.x + s1.y);
+}
+
+// The same reduction for two queries at once (HQ = 8, "pair" TMEM layout): v[4g + o],
+// v[4g + o + 1] are head g of queries (a, b); w[g] = (w_a[g], w_b[g]).  Packed
+// accumulator A_i holds heads (i, i + 4) of both queries, exactly the fma chains of
+// gate_relu4's s0.x / s0.y / s1.x / s1.y, so .x / .y are bit-identical to
+// gate_relu_finish of query a / b.
+__device__ __forceinline__ float2 gate_relu_pair8(const uint32_t* v, int o, const float2 (&w)[8]) {
+  float2 A[4];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const float2 x = make_float2(fmaxf(__uint_as_float(v[4 * g + o]), 0.f), fmaxf(__uint_as_float(v[4 * g + o + 1]), 0.f));
+    A[g & 3] = __ffma2_rn(w[g], x, g < 4 ? make_float2(0.f, 0.f) : A[g & 3]);
+  }
+  return __fadd2_rn(__fadd2_rn(A[0], A[1]), __fadd2_rn(A[2], A[3]));
 }
 }  // namespace misa

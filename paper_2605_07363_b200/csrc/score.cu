@@ -81,6 +81,38 @@ __device__ __forceinline__ void reduce_all(const uint32_t* r, const float* __res
   }
 }
 
+// FILTER append of one 32-key warp slice: per query one ballot; passing lanes store
+// (score bits, key) at their rank after the list's running count (ascending keys).
+template <int QW, bool EDGE>
+__device__ __forceinline__ void append(const float (&sc)[QW], int key, const float* sTau, const int* sLim,
+                                       uint64_t* dst0, uint32_t qs, int (&cnt)[QW], uint32_t lt, int cap) {
+#pragma unroll
+  for (int q = 0; q < QW; ++q) {
+    bool pass = sc[q] >= sTau[q];
+    if constexpr (EDGE) pass = pass && key < sLim[q];
+    const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+    const int pos = cnt[q] + __popc(bal & lt);
+    ptx::st_global_v2_idx_if(dst0, q * qs + static_cast<uint32_t>(pos), __float_as_uint(sc[q]),
+                             static_cast<uint32_t>(key), pass && pos < cap);
+    cnt[q] += __popc(bal);
+  }
+}
+
+// Tile column r <-> (query within the item, head slot).  HQ = 8 uses the "pair"
+// order (column 8g + q%8 of 64-column slab q/8 is head g of query q), so that a
+// 16x256b TMEM load hands every thread all 8 heads of two queries (see gate_relu_pair8);
+// other widths are query-major (r = q*HQ + j).
+template <int HQ>
+__device__ __forceinline__ int col_query(int r) {
+  if constexpr (HQ == 8) return (r >> 6) * 8 + (r & 7);
+  else return r / HQ;
+}
+template <int HQ>
+__device__ __forceinline__ int col_head(int r) {
+  if constexpr (HQ == 8) return (r >> 3) & 7;
+  else return r % HQ;
+}
+
 struct ScoreArgs {
   const __nv_bfloat16* __restrict__ q;  // [T][Hp][D]
   const float* __restrict__ w;          // [T][Hp]
@@ -249,7 +281,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
       constexpr int CH = D / 8;  // 16-byte chunks per row
       for (int c = et; c < kTileCols * CH; c += EPI_THREADS) {
         const int r = c / CH, ch = c - r * CH;
-        const int qi = r / HQ, j = r - qi * HQ;
+        const int qi = col_query<HQ>(r), j = col_head<HQ>(r);
         const int row = row0 + qi;
         int head = -1;
         if (row < a.T) head = a.heads ? a.heads[(int64_t)row * HQ + j] : (j < a.H ? j : -1);
@@ -258,7 +290,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         *reinterpret_cast<uint4*>(sB + ptx::sw128_offset(r, ch * 8, C::B_ATOM)) = v;
       }
       for (int r = et; r < kTileCols; r += EPI_THREADS) {
-        const int qi = r / HQ, j = r - qi * HQ;
+        const int qi = col_query<HQ>(r), j = col_head<HQ>(r);
         const int row = row0 + qi;
         float wv = 0.f;
         if (row < a.T) {
@@ -283,82 +315,155 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
       ptx::named_bar_sync(1, EPI_THREADS);
       if (et == 0) ptx::mbar_arrive(bfull);
 
-      const int qbase = split * QW;  // first query row (within the item) of this warp
-      int lim_min = 0x7fffffff;
+      if constexpr (HQ == 8) {
+        // ---- pair layout: thread (rr = lane/4, m = lane%4) owns keys quad*32 + rr + 8s
+        // (s = 0..3) of queries qa = split*8 + 2m and qa + 1, with all their 8 gate
+        // weights in registers for the whole item (no shared-memory reads per tile).
+        const int m = lane & 3, rr = lane >> 2;
+        const int qa = split * 8 + 2 * m;
+        float2 wp[8];
 #pragma unroll
-      for (int q = 0; q < QW; ++q) lim_min = min(lim_min, sLim[qbase + q]);
-      const float* wcol = sW + split * C::COLS;
-      // FILTER: cnt[q] is the (warp-uniform) number of candidates of query qbase+q
-      // this warp has appended so far; lists stay in ascending key order.
-      int cnt[QW];
+        for (int g = 0; g < 8; ++g) wp[g] = *reinterpret_cast<const float2*>(sW + split * 64 + 8 * g + 2 * m);
+        const float tau_a = sTau[qa], tau_b = sTau[qa + 1];
+        int lim_min = 0x7fffffff;
 #pragma unroll
-      for (int q = 0; q < QW; ++q) cnt[q] = 0;
-      const uint32_t lt = ptx::lanemask_lt();
-      uint64_t* dst0 = nullptr;
-      const int qstride = kQuadrants * a.cap;  // elements between consecutive rows' lists
-      if (FILTER) dst0 = a.cand + (static_cast<int64_t>(row0 + qbase) * kQuadrants + quad) * a.cap;
-      for (int jt = 0; jt < nt; ++jt) {
-        ptx::mbar_wait(&tfull[acc], aph);
-        ptx::tc_fence_after();
-        const int key0 = jt * kTileKeys + quad * 32;
-        const int key = key0 + lane;
-        const uint32_t taddr =
-            tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols + split * C::COLS;
-        float sc[QW];
-        float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
-        if constexpr (C::COLS <= 64) {
-          // whole column slice in registers at once: the accumulator buffer is handed
-          // back to the MMA warp before any arithmetic, so the tensor pipe never waits
-          // on the epilogue's latency, only on its throughput.
-          uint32_t r[C::COLS];
-#pragma unroll
-          for (int c = 0; c < C::COLS; c += 32) ptx::tmem_ld_x32p(taddr + c, r + c);
-#pragma unroll
-          for (int c = 0; c < C::COLS; c += 32) ptx::tmem_wait_ld_dep32p(r + c);
+        for (int q = 0; q < 8; ++q) lim_min = min(lim_min, sLim[split * 8 + q]);
+        const uint32_t gm = 0x11111111u << m;  // lanes of this query pair
+        const uint32_t lm = gm & ptx::lanemask_lt();
+        int cnt_a = 0, cnt_b = 0;
+        uint64_t* dst = nullptr;
+        if (FILTER) dst = a.cand + (static_cast<int64_t>(row0 + qa) * kQuadrants + quad) * a.cap;
+        const uint32_t qs = kQuadrants * a.cap;
+        for (int jt = 0; jt < nt; ++jt) {
+          ptx::mbar_wait(&tfull[acc], aph);
+          ptx::tc_fence_after();
+          const uint32_t taddr =
+              tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols + split * 64;
+          uint32_t v0[32], v1[32];
+          ptx::tmem_ld_16x256b_x8(taddr, v0);
+          ptx::tmem_ld_16x256b_x8(taddr + (16u << 16), v1);
+          ptx::tmem_wait_ld_dep32p(v0);
+          ptx::tmem_wait_ld_dep32p(v1);
           ptx::tc_fence_before();
           ptx::mbar_arrive(&tempty[acc]);
-          reduce_all<HQ, QW, C::NCH, 0>(r, wcol, sc, p0, p1);
-        } else {
-          uint32_t ra[16], rb[16];
-          ptx::tmem_ld_x16(taddr, ra);
-          ptx::tmem_wait_ld_dep16(ra);
-          drain<HQ, QW, C::NCH, 0>(taddr, wcol, sc, p0, p1, ra, rb);
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty[acc]);
-        }
-        if (++acc == 2) { acc = 0; aph ^= 1; }
-
-        if constexpr (FILTER) {
-          // one ballot per query: passing lanes write at (count so far + rank among the
-          // warp's passing lanes), so no staging, no serial loop and no divergence.
-          // The prefix bound is only tested on the warp's last (diagonal) tile.
-          const bool edge = key0 + 31 >= lim_min;
-          const uint64_t khi = static_cast<uint64_t>(static_cast<uint32_t>(key)) << 32;
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+          float2 sc[4];
+          sc[0] = gate_relu_pair8(v0, 0, wp);
+          sc[1] = gate_relu_pair8(v0, 2, wp);
+          sc[2] = gate_relu_pair8(v1, 0, wp);
+          sc[3] = gate_relu_pair8(v1, 2, wp);
+          const int kq = jt * kTileKeys + quad * 32;
+          if constexpr (FILTER) {
+            const bool edge = kq + 31 >= lim_min;  // warp-uniform
 #pragma unroll
-          for (int q = 0; q < QW; ++q) {
-            bool pass = sc[q] >= sTau[qbase + q];
-            if (edge) pass = pass && key < sLim[qbase + q];
-            const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-            const int pos = cnt[q] + __popc(bal & lt);
-            ptx::st_global_u64_if(dst0 + static_cast<uint32_t>(q * qstride + pos), khi | __float_as_uint(sc[q]),
-                                  pass && pos < a.cap);
-            cnt[q] += __popc(bal);
+            for (int s4 = 0; s4 < 4; ++s4) {
+              const int key = kq + rr + 8 * s4;
+#pragma unroll
+              for (int b = 0; b < 2; ++b) {
+                const float v = b ? sc[s4].y : sc[s4].x;
+                bool pass = v >= (b ? tau_b : tau_a);
+                if (edge) pass = pass && key < sLim[qa + b];
+                const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+                int& cnt = b ? cnt_b : cnt_a;
+                const int pos = cnt + __popc(bal & lm);
+                ptx::st_global_v2_idx_if(dst, b * qs + static_cast<uint32_t>(pos), __float_as_uint(v),
+                                         static_cast<uint32_t>(key), pass && pos < a.cap);
+                cnt += __popc(bal & gm);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const int lim = sLim[qa + b];
+              float* o = a.out + static_cast<int64_t>(row0 + qa + b) * a.out_ld;
+#pragma unroll
+              for (int s4 = 0; s4 < 4; ++s4) {
+                const int key = kq + rr + 8 * s4;
+                if (key < lim) o[key] = b ? sc[s4].y : sc[s4].x;
+              }
+            }
           }
-        } else {
-          float* o = a.out + static_cast<int64_t>(row0 + qbase) * a.out_ld + key;
-#pragma unroll
-          for (int q = 0; q < QW; ++q)
-            if (key < sLim[qbase + q]) o[q * a.out_ld] = sc[q];
         }
-      }
-      if constexpr (FILTER) {
-        int mine = 0;
+        if constexpr (FILTER) {
+          if (rr == 0) {
 #pragma unroll
-        for (int q = 0; q < QW; ++q)
-          if (lane == q) mine = cnt[q];
-        if (lane < QW) {
-          const int row = row0 + qbase + lane;
-          if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = mine;
+            for (int b = 0; b < 2; ++b) {
+              const int row = row0 + qa + b;
+              if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = b ? cnt_b : cnt_a;
+            }
+          }
+        }
+      } else {
+        const int qbase = split * QW;  // first query row (within the item) of this warp
+        int lim_min = 0x7fffffff;
+  #pragma unroll
+        for (int q = 0; q < QW; ++q) lim_min = min(lim_min, sLim[qbase + q]);
+        const float* wcol = sW + split * C::COLS;
+        // FILTER: cnt[q] is the (warp-uniform) number of candidates of query qbase+q
+        // this warp has appended so far; lists stay in ascending key order.
+        int cnt[QW];
+  #pragma unroll
+        for (int q = 0; q < QW; ++q) cnt[q] = 0;
+        const uint32_t lt = ptx::lanemask_lt();
+        // list of query qbase+q = dst0 + q * qs (rows past T are never written: limit 0)
+        uint64_t* dst0 = nullptr;
+        if (FILTER) dst0 = a.cand + (static_cast<int64_t>(row0 + qbase) * kQuadrants + quad) * a.cap;
+        const uint32_t qs = kQuadrants * a.cap;
+        for (int jt = 0; jt < nt; ++jt) {
+          ptx::mbar_wait(&tfull[acc], aph);
+          ptx::tc_fence_after();
+          const int key0 = jt * kTileKeys + quad * 32;
+          const int key = key0 + lane;
+          const uint32_t taddr =
+              tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols + split * C::COLS;
+          float sc[QW];
+          float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
+          if constexpr (C::COLS <= 64) {
+            // whole column slice in registers at once: the accumulator buffer is handed
+            // back to the MMA warp before any arithmetic, so the tensor pipe never waits
+            // on the epilogue's latency, only on its throughput.
+            uint32_t r[C::COLS];
+  #pragma unroll
+            for (int c = 0; c < C::COLS; c += 32) ptx::tmem_ld_x32p(taddr + c, r + c);
+  #pragma unroll
+            for (int c = 0; c < C::COLS; c += 32) ptx::tmem_wait_ld_dep32p(r + c);
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+            reduce_all<HQ, QW, C::NCH, 0>(r, wcol, sc, p0, p1);
+          } else {
+            uint32_t ra[16], rb[16];
+            ptx::tmem_ld_x16(taddr, ra);
+            ptx::tmem_wait_ld_dep16(ra);
+            drain<HQ, QW, C::NCH, 0>(taddr, wcol, sc, p0, p1, ra, rb);
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+          }
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+
+          if constexpr (FILTER) {
+            // one ballot per query: passing lanes write at (count so far + rank among the
+            // warp's passing lanes), so no staging, no serial loop and no divergence.
+            // The prefix bound is only tested on the warp's diagonal tile (warp-uniform).
+            if (key0 + 31 >= lim_min)
+              append<QW, true>(sc, key, sTau + qbase, sLim + qbase, dst0, qs, cnt, lt, a.cap);
+            else
+              append<QW, false>(sc, key, sTau + qbase, sLim + qbase, dst0, qs, cnt, lt, a.cap);
+          } else {
+            float* o = a.out + static_cast<int64_t>(row0 + qbase) * a.out_ld + key;
+  #pragma unroll
+            for (int q = 0; q < QW; ++q)
+              if (key < sLim[qbase + q]) o[q * a.out_ld] = sc[q];
+          }
+        }
+        if constexpr (FILTER) {
+          int mine = 0;
+  #pragma unroll
+          for (int q = 0; q < QW; ++q)
+            if (lane == q) mine = cnt[q];
+          if (lane < QW) {
+            const int row = row0 + qbase + lane;
+            if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = mine;
+          }
         }
       }
       ptx::named_bar_sync(1, EPI_THREADS);
