@@ -21,7 +21,7 @@
 //               accumulator, ReLU * w * sum (packed FFMA2) -> either store
 //               the score row (MATERIALIZE) or append (score, key) >= tau to the
 //               row's per-quadrant candidate list (FILTER: the fused top-k's
-//               candidate pass; lists stay in ascending key order).
+//               candidate pass; each list in ascending key order, no cross-warp sync).
 //
 // A work item is a group of G consecutive query rows scanning key tiles
 // [0, ceil(max_t lim_t / 128)) — causal rows skip every tile past their prefix.
@@ -81,20 +81,31 @@ __device__ __forceinline__ void reduce_all(const uint32_t* r, const float* __res
   }
 }
 
-// FILTER append of one 32-key warp slice: per query one ballot; passing lanes store
-// (score bits, key) at their rank after the list's running count (ascending keys).
+// FILTER pass masks of one 32-key warp slice (lane = key): one ballot per query.
 template <int QW, bool EDGE>
-__device__ __forceinline__ void append(const float (&sc)[QW], int key, const float* sTau, const int* sLim,
-                                       uint64_t* dst0, uint32_t qs, int (&cnt)[QW], uint32_t lt, int cap) {
+__device__ __forceinline__ void pass_ballots(const float (&sc)[QW], int key, const float* sTau, const int* sLim,
+                                             uint32_t (&bal)[QW]) {
 #pragma unroll
   for (int q = 0; q < QW; ++q) {
     bool pass = sc[q] >= sTau[q];
     if constexpr (EDGE) pass = pass && key < sLim[q];
-    const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-    const int pos = cnt[q] + __popc(bal & lt);
-    ptx::st_global_v2_idx_if(dst0, q * qs + static_cast<uint32_t>(pos), __float_as_uint(sc[q]),
-                             static_cast<uint32_t>(key), pass && pos < cap);
-    cnt[q] += __popc(bal);
+    bal[q] = __ballot_sync(0xffffffffu, pass);
+  }
+}
+
+// Pair layout: ballots of the 4 key slots (key = key0 + 8*s) x 2 queries (a, b).
+template <bool EDGE>
+__device__ __forceinline__ void pair_ballots(const float2 (&sc)[4], int key0, float tau_a, float tau_b,
+                                             const int* sLim, uint32_t (&bal)[4][2]) {
+#pragma unroll
+  for (int s4 = 0; s4 < 4; ++s4) {
+    bool pa = sc[s4].x >= tau_a, pb = sc[s4].y >= tau_b;
+    if constexpr (EDGE) {
+      pa = pa && key0 + 8 * s4 < sLim[0];
+      pb = pb && key0 + 8 * s4 < sLim[1];
+    }
+    bal[s4][0] = __ballot_sync(0xffffffffu, pa);
+    bal[s4][1] = __ballot_sync(0xffffffffu, pb);
   }
 }
 
@@ -330,8 +341,8 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         for (int q = 0; q < 8; ++q) lim_min = min(lim_min, sLim[split * 8 + q]);
         const uint32_t gm = 0x11111111u << m;  // lanes of this query pair
         const uint32_t lm = gm & ptx::lanemask_lt();
-        int cnt_a = 0, cnt_b = 0;
-        uint64_t* dst = nullptr;
+        int cnt_a = 0, cnt_b = 0;  // candidates of rows qa / qa+1 appended by this warp
+        uint64_t* dst = nullptr;   // list of (row, quad) = cand[(row*4 + quad) * cap]
         if (FILTER) dst = a.cand + (static_cast<int64_t>(row0 + qa) * kQuadrants + quad) * a.cap;
         const uint32_t qs = kQuadrants * a.cap;
         for (int jt = 0; jt < nt; ++jt) {
@@ -354,21 +365,22 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
           sc[3] = gate_relu_pair8(v1, 2, wp);
           const int kq = jt * kTileKeys + quad * 32;
           if constexpr (FILTER) {
-            const bool edge = kq + 31 >= lim_min;  // warp-uniform
+            uint32_t bal[4][2];
+            if (kq + 31 >= lim_min)  // warp-uniform: only the diagonal tile tests the prefix bound
+              pair_ballots<true>(sc, kq + rr, tau_a, tau_b, sLim + qa, bal);
+            else
+              pair_ballots<false>(sc, kq + rr, tau_a, tau_b, sLim + qa, bal);
 #pragma unroll
             for (int s4 = 0; s4 < 4; ++s4) {
-              const int key = kq + rr + 8 * s4;
+              const uint32_t key = static_cast<uint32_t>(kq + rr + 8 * s4);
 #pragma unroll
               for (int b = 0; b < 2; ++b) {
-                const float v = b ? sc[s4].y : sc[s4].x;
-                bool pass = v >= (b ? tau_b : tau_a);
-                if (edge) pass = pass && key < sLim[qa + b];
-                const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+                const uint32_t bl = bal[s4][b];
                 int& cnt = b ? cnt_b : cnt_a;
-                const int pos = cnt + __popc(bal & lm);
-                ptx::st_global_v2_idx_if(dst, b * qs + static_cast<uint32_t>(pos), __float_as_uint(v),
-                                         static_cast<uint32_t>(key), pass && pos < a.cap);
-                cnt += __popc(bal & gm);
+                const int pos = cnt + __popc(bl & lm);
+                ptx::st_global_v2_idx_if(dst, b * qs + pos, __float_as_uint(b ? sc[s4].y : sc[s4].x), key,
+                                         ((bl >> lane) & 1u) && pos < a.cap);
+                cnt += __popc(bl & gm);
               }
             }
           } else {
@@ -399,14 +411,12 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
   #pragma unroll
         for (int q = 0; q < QW; ++q) lim_min = min(lim_min, sLim[qbase + q]);
         const float* wcol = sW + split * C::COLS;
-        // FILTER: cnt[q] is the (warp-uniform) number of candidates of query qbase+q
-        // this warp has appended so far; lists stay in ascending key order.
+        // FILTER: cnt[q] = candidates of query qbase+q appended by this warp (warp-uniform)
         int cnt[QW];
   #pragma unroll
         for (int q = 0; q < QW; ++q) cnt[q] = 0;
         const uint32_t lt = ptx::lanemask_lt();
-        // list of query qbase+q = dst0 + q * qs (rows past T are never written: limit 0)
-        uint64_t* dst0 = nullptr;
+        uint64_t* dst0 = nullptr;  // list of query qbase+q = dst0 + q * qs
         if (FILTER) dst0 = a.cand + (static_cast<int64_t>(row0 + qbase) * kQuadrants + quad) * a.cap;
         const uint32_t qs = kQuadrants * a.cap;
         for (int jt = 0; jt < nt; ++jt) {
@@ -441,13 +451,18 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
           if (++acc == 2) { acc = 0; aph ^= 1; }
 
           if constexpr (FILTER) {
-            // one ballot per query: passing lanes write at (count so far + rank among the
-            // warp's passing lanes), so no staging, no serial loop and no divergence.
-            // The prefix bound is only tested on the warp's diagonal tile (warp-uniform).
-            if (key0 + 31 >= lim_min)
-              append<QW, true>(sc, key, sTau + qbase, sLim + qbase, dst0, qs, cnt, lt, a.cap);
+            uint32_t bal[QW];
+            if (key0 + 31 >= lim_min)  // the prefix bound only matters on the diagonal tile
+              pass_ballots<QW, true>(sc, key, sTau + qbase, sLim + qbase, bal);
             else
-              append<QW, false>(sc, key, sTau + qbase, sLim + qbase, dst0, qs, cnt, lt, a.cap);
+              pass_ballots<QW, false>(sc, key, sTau + qbase, sLim + qbase, bal);
+  #pragma unroll
+            for (int q = 0; q < QW; ++q) {
+              const int pos = cnt[q] + __popc(bal[q] & lt);
+              ptx::st_global_v2_idx_if(dst0, q * qs + pos, __float_as_uint(sc[q]), static_cast<uint32_t>(key),
+                                       ((bal[q] >> lane) & 1u) && pos < a.cap);
+              cnt[q] += __popc(bal[q]);
+            }
           } else {
             float* o = a.out + static_cast<int64_t>(row0 + qbase) * a.out_ld + key;
   #pragma unroll

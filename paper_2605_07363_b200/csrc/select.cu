@@ -42,6 +42,10 @@ struct SelSh {
   int wtot[NW];
   int lst_off[kMaxLists + 1];
   int lst_sel[kMaxLists + 1];
+  uint32_t hist[2048];  // histogram cut: bins of (key - lo) >> shift
+  uint32_t rmin[NW], rmax[NW];
+  int hscan[NW];
+  int hb_bin, hb_above, hb_count;
   uint32_t bkey[256];  // boundary bucket (exact cut) staging
   int32_t bidx[256];
   int bcount;
@@ -399,6 +403,136 @@ __device__ void v3_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N, i
   thr_out = (need < bucket) ? static_cast<int>(~t2) : 0x7fffffff;
 }
 
+// ------------------------------------------- histogram cut (v4) ----
+// The (score desc, index asc) cut of the kk-th element: bins of the valid keys' range
+// [lo, hi] at 11-bit resolution (2048 bins, one smem atomic per element), one block
+// scan from the top bin to the boundary bin, refined by another level only when that
+// bin still holds more than kBucketMax elements; the boundary bin's elements are then
+// ranked exactly by (key desc, index asc) with one element per thread.
+template <int NT, int EPT>
+__device__ void hist_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N, int kk, SelSh<NT>& sh,
+                         int& parity, uint32_t& v_out, int& thr_out) {
+  constexpr int NW = NT / 32;
+  constexpr int NB = 2048, BPT = NB / NT;  // bins per thread
+  static_assert(NB % NT == 0 && BPT >= 1 && BPT <= 16, "bins per thread");
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    if (key[r]) {
+      mn = min(mn, key[r]);
+      mx = max(mx, key[r]);
+    }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) {
+    sh.rmin[w] = mn;
+    sh.rmax[w] = mx;
+  }
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) sh.hist[tid * BPT + i] = 0u;
+  __syncthreads();
+  mn = sh.rmin[0];
+  mx = sh.rmax[0];
+#pragma unroll
+  for (int i = 1; i < NW; ++i) {
+    mn = min(mn, sh.rmin[i]);
+    mx = max(mx, sh.rmax[i]);
+  }
+  // level window: keys in [lo, lo + span) with span - 1 <= 0xffffffff, bins of 2^sft
+  uint32_t lo = mn, span_m1 = mx - mn;
+  int sft = span_m1 == 0u ? 0 : max(0, 32 - __clz(span_m1) - 11);
+  int need = kk, cB;
+  for (;;) {
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const uint32_t d = key[r] - lo;
+      if (key[r] && d <= span_m1) atomicAdd(&sh.hist[d >> sft], 1u);
+    }
+    __syncthreads();
+    // thread tid owns bins [NB - BPT*(tid+1), NB - BPT*tid): descending key order
+    uint32_t c[BPT];
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+      c[i] = sh.hist[NB - 1 - (tid * BPT + i)];
+      tot += static_cast<int>(c[i]);
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) sh.hscan[w] = incl;
+    __syncthreads();
+    int above = incl - tot;
+    for (int i = 0; i < w; ++i) above += sh.hscan[i];
+    if (above < need && need <= above + tot) {
+#pragma unroll
+      for (int i = 0; i < BPT; ++i) {
+        if (above < need && need <= above + static_cast<int>(c[i])) {
+          sh.hb_bin = NB - 1 - (tid * BPT + i);
+          sh.hb_above = above;
+          sh.hb_count = static_cast<int>(c[i]);
+        }
+        above += static_cast<int>(c[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) sh.hist[tid * BPT + i] = 0u;  // ready for a next level
+    if (tid == 0) sh.bcount = 0;
+    __syncthreads();
+    const int B = sh.hb_bin;
+    need -= sh.hb_above;
+    cB = sh.hb_count;
+    lo += static_cast<uint32_t>(B) << sft;
+    span_m1 = sft == 0 ? 0u : ((1u << sft) - 1u);
+    if (cB <= kBucketMax || sft == 0) break;
+    sft = max(0, sft - 11);
+  }
+  // elements of the boundary bin: keys in [lo, lo + span_m1]
+  if (cB <= kBucketMax) {
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      if (key[r] && key[r] - lo <= span_m1) {
+        const int p = atomicAdd(&sh.bcount, 1);
+        sh.bkey[p] = key[r];
+        sh.bidx[p] = sidx[v3_elem<NT, EPT>(r)];
+      }
+    }
+    __syncthreads();
+    // exact rank of each boundary element under (key desc, index asc); the one with
+    // rank need-1 is the cut
+    for (int e = tid; e < cB; e += NT) {
+      const uint32_t ke = sh.bkey[e];
+      const int ie = sh.bidx[e];
+      int rank = 0;
+      for (int f = 0; f < cB; ++f) {
+        const uint32_t kf = sh.bkey[f];
+        rank += (kf > ke) || (kf == ke && sh.bidx[f] < ie);
+      }
+      if (rank == need - 1) {
+        sh.res_v = ke;
+        sh.res_thr = ie;
+      }
+    }
+    __syncthreads();
+    v_out = sh.res_v;
+    thr_out = sh.res_thr;
+    __syncthreads();
+    return;
+  }
+  // more than kBucketMax copies of one key value: keep the `need` smallest indices
+  int c2, c3;
+  const uint32_t t2 = kth_largest<NT, EPT>(
+      [&](int r) { return (key[r] == lo) ? ~static_cast<uint32_t>(sidx[v3_elem<NT, EPT>(r)]) : 0u; }, need, sh,
+      parity, &c2, &c3);
+  v_out = lo;
+  thr_out = (need < cB) ? static_cast<int>(~t2) : 0x7fffffff;
+}
+
 // Select the kk best of the N staged elements (NL lists, each ascending by index,
 // offsets in sh.lst_off) and write them ascending to out[0..kk) (+ scores), -1 pad.
 template <int NT, int EPT>
@@ -409,7 +543,7 @@ __device__ void v3_select(const uint32_t (&key)[EPT], const int32_t* sidx, int N
   int parity = 0;
   uint32_t v = 0;
   int thr = 0x7fffffff;
-  if (kk < N) v3_cut<NT, EPT>(key, sidx, N, kk, sh, parity, v, thr);
+  if (kk < N) hist_cut<NT, EPT>(key, sidx, N, kk, sh, parity, v, thr);
   uint32_t selm = 0;
   int cnt = 0;
 #pragma unroll
