@@ -693,17 +693,22 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) topk_kernel(const uin
   float* csc = reinterpret_cast<float*>(cidx + 2 * k);
   const uint64_t* rowc = cand + (int64_t)t * kQuadrants * cap;
   auto load = [&](auto& key, int32_t* si) {
+    // all loads issued before any use (branch-free, clamped in-bounds addresses), so a
+    // row costs one memory latency instead of one per slot
     constexpr int E = sizeof(key) / sizeof(key[0]);
+    uint2 rw[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       const int e = v3_elem<NT, E>(r);
-      uint2 rw = make_uint2(0u, 0u);
-      if (e < total) {
-        const int q = (e >= off[1]) + (e >= off[2]) + (e >= off[3]);
-        rw = *reinterpret_cast<const uint2*>(rowc + (int64_t)q * cap + (e - off[q]));
-        si[e] = static_cast<int32_t>(rw.y);
-      }
-      key[r] = e < total ? float_key(__uint_as_float(rw.x)) : 0u;
+      const int q = (e >= off[1]) + (e >= off[2]) + (e >= off[3]);
+      const int64_t at = e < total ? (int64_t)q * cap + (e - off[q]) : 0;
+      rw[r] = __ldcs(reinterpret_cast<const uint2*>(rowc + at));
+    }
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int e = v3_elem<NT, E>(r);
+      if (e < total) si[e] = static_cast<int32_t>(rw[r].y);
+      key[r] = e < total ? float_key(__uint_as_float(rw[r].x)) : 0u;
     }
   };
   if (kk <= 0) {
@@ -750,11 +755,20 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
   float* csc = reinterpret_cast<float*>(cidx + 2 * k);
   auto load = [&](auto& key, int32_t* si) {
     constexpr int E = sizeof(key) / sizeof(key[0]);
+    float x[E];
+    int32_t ix[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       const int e = v3_elem<NT, E>(r);
-      key[r] = e < n ? float_key(row[e]) : 0u;
-      if (e < n) si[e] = irow ? irow[e] : e;
+      const int ec = e < n ? e : 0;
+      x[r] = row[ec];
+      ix[r] = irow ? irow[ec] : e;
+    }
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int e = v3_elem<NT, E>(r);
+      key[r] = e < n ? float_key(x[r]) : 0u;
+      if (e < n) si[e] = ix[r];
     }
   };
   v3_dispatch<NT, EPT>(n, load, 1, kk, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
