@@ -117,10 +117,11 @@ int misa_select_threshold(const float* sample_scores, int64_t ld, const int32_t*
  * Rows with n_t <= k select [0, n_t) (without scores; when topk_scores is requested such
  * rows are selected from their candidates instead, which must then hold every key).
  * topk_scores (optional) holds the scores aligned with topk.  flags[t] gets MISA_FLAG_*
- * on overflow / underflow (row left -1). */
+ * on overflow / underflow (row left -1).  max_prefix_len (an upper bound of prefix_len, or 0
+ * when unknown) lets the merge-free chunk-ordered selector size its staging. */
 int misa_select_topk(const uint64_t* cand, const int32_t* cand_count, int cap, const int32_t* prefix_len,
-                     int64_t n_rows, int k, int32_t* topk, int64_t topk_ld, float* topk_scores, int32_t* flags,
-                     void* stream);
+                     int64_t n_rows, int k, int64_t max_prefix_len, int32_t* topk, int64_t topk_ld,
+                     float* topk_scores, int32_t* flags, void* stream);
 
 /* Exact top-k over dense rows: value scores[r*ld + i] for i < row_len[r] with index
  * idx[r*idx_ld + i] (or i when idx == NULL); rows listed in rows[] (or all when NULL). */

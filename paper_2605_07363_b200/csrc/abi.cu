@@ -69,6 +69,6 @@ int sm_count() {
 
 }  // namespace misa
 
-extern "C" int misa_abi_version(void) { return 1; }
+extern "C" int misa_abi_version(void) { return 2; }
 extern "C" const char* misa_last_error(void) { return misa::g_err; }
 extern "C" int misa_sm_count(void) { return misa::sm_count(); }

@@ -23,6 +23,8 @@
 // misa_select_dense      a dense (optionally index-listed) row; rows too long for
 //                        registers take a global-memory radix path (exact fallback)
 // misa_merge_topk        the gathered per-GPU top-k lists of a row
+#include <algorithm>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -46,6 +48,7 @@ struct SelSh {
   uint32_t rmin[NW], rmax[NW];
   int hscan[NW];
   int hb_bin, hb_above, hb_count;
+  int lst_g[kMaxLists + 1];  // v5: compacted rank of each list's first selected element
   uint32_t bkey[256];  // boundary bucket (exact cut) staging
   int32_t bidx[256];
   int bcount;
@@ -409,9 +412,9 @@ __device__ void v3_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N, i
 // scan from the top bin to the boundary bin, refined by another level only when that
 // bin still holds more than kBucketMax elements; the boundary bin's elements are then
 // ranked exactly by (key desc, index asc) with one element per thread.
-template <int NT, int EPT>
-__device__ void hist_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N, int kk, SelSh<NT>& sh,
-                         int& parity, uint32_t& v_out, int& thr_out) {
+template <int NT, int EPT, typename IdxFn>
+__device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk, SelSh<NT>& sh, int& parity,
+                         uint32_t& v_out, int& thr_out) {
   constexpr int NW = NT / 32;
   constexpr int NB = 2048, BPT = NB / NT;  // bins per thread
   static_assert(NB % NT == 0 && BPT >= 1 && BPT <= 16, "bins per thread");
@@ -499,7 +502,7 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N,
       if (key[r] && key[r] - lo <= span_m1) {
         const int p = atomicAdd(&sh.bcount, 1);
         sh.bkey[p] = key[r];
-        sh.bidx[p] = sidx[v3_elem<NT, EPT>(r)];
+        sh.bidx[p] = idx_of(r);
       }
     }
     __syncthreads();
@@ -527,8 +530,7 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N,
   // more than kBucketMax copies of one key value: keep the `need` smallest indices
   int c2, c3;
   const uint32_t t2 = kth_largest<NT, EPT>(
-      [&](int r) { return (key[r] == lo) ? ~static_cast<uint32_t>(sidx[v3_elem<NT, EPT>(r)]) : 0u; }, need, sh,
-      parity, &c2, &c3);
+      [&](int r) { return (key[r] == lo) ? ~static_cast<uint32_t>(idx_of(r)) : 0u; }, need, sh, parity, &c2, &c3);
   v_out = lo;
   thr_out = (need < cB) ? static_cast<int>(~t2) : 0x7fffffff;
 }
@@ -543,7 +545,8 @@ __device__ void v3_select(const uint32_t (&key)[EPT], const int32_t* sidx, int N
   int parity = 0;
   uint32_t v = 0;
   int thr = 0x7fffffff;
-  if (kk < N) hist_cut<NT, EPT>(key, sidx, N, kk, sh, parity, v, thr);
+  if (kk < N)
+    hist_cut<NT, EPT>(key, [&](int r) { return sidx[v3_elem<NT, EPT>(r)]; }, N, kk, sh, parity, v, thr);
   uint32_t selm = 0;
   int cnt = 0;
 #pragma unroll
@@ -650,76 +653,342 @@ __device__ void v3_dispatch(int N, LoadFn load, int NL, int kk, SelSh<NT>& sh, i
 }
 
 // -------------------------------------------------- candidates -> top-k ----
-template <int NT, int EPT>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) topk_kernel(const uint64_t* __restrict__ cand,
+// Persistent: CTA b handles rows b, b + grid, ...  The next row's 4 quadrant lists
+// are bulk-copied (cp.async.bulk, mbarrier complete_tx) into shared memory while the
+// current row is being cut, selected and merged, so no row waits on DRAM latency.
+struct TopkPrefetch {
+  int row, n, c[kQuadrants];
+  bool copy;  // lists in flight (false: row needs no candidates or is past the end)
+};
+
+template <int NT, int EPT, bool PF>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uint64_t* __restrict__ cand,
                                                   const int32_t* __restrict__ cand_count, int cap,
-                                                  const int32_t* __restrict__ prefix_len, int k,
+                                                  const int32_t* __restrict__ prefix_len, int n_rows, int k,
                                                   int32_t* __restrict__ topk, int64_t topk_ld,
                                                   float* __restrict__ topk_scores, int32_t* __restrict__ flags) {
-  extern __shared__ __align__(16) uint8_t dsm[];
+  extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ SelSh<NT> sh;
-  const int t = blockIdx.x;
-  const int n = prefix_len[t];
-  int32_t* out = topk + (int64_t)t * topk_ld;
-  float* outs = topk_scores ? topk_scores + (int64_t)t * topk_ld : nullptr;
-  const int kk = n < k ? n : k;
-  if (n <= k && !outs) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73)
-    for (int i = threadIdx.x; i < k; i += NT) {
-      out[i] = i < n ? i : -1;
-      if (outs && i >= n) outs[i] = -INFINITY;
-    }
-    if (threadIdx.x == 0 && flags) flags[t] = 0;
-    return;
-  }
-  int off[kQuadrants + 1];
-  bool overflow = false;
-  off[0] = 0;
-#pragma unroll
-  for (int q = 0; q < kQuadrants; ++q) {
-    const int c = cand_count[(int64_t)t * kQuadrants + q];
-    overflow |= c > cap;
-    off[q + 1] = off[q] + (c < cap ? c : cap);
-  }
-  const int total = off[kQuadrants];
-  if (overflow || total < kk || total > NT * EPT) {
-    for (int i = threadIdx.x; i < k; i += NT) out[i] = -1;
-    if (threadIdx.x == 0 && flags)
-      flags[t] = (overflow || total > NT * EPT) ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
-    return;
-  }
-  if (threadIdx.x <= kQuadrants) sh.lst_off[threadIdx.x] = off[threadIdx.x];
-  int32_t* sidx = reinterpret_cast<int32_t*>(dsm);
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ TopkPrefetch pf;
+  uint64_t* raw = reinterpret_cast<uint64_t*>(dsm);  // PF: list q at raw + q*cap
+  int32_t* sidx = reinterpret_cast<int32_t*>(raw + (PF ? (size_t)kQuadrants * cap : 0));
   int32_t* cidx = sidx + NT * EPT;
   float* csc = reinterpret_cast<float*>(cidx + 2 * k);
-  const uint64_t* rowc = cand + (int64_t)t * kQuadrants * cap;
-  auto load = [&](auto& key, int32_t* si) {
-    // all loads issued before any use (branch-free, clamped in-bounds addresses), so a
-    // row costs one memory latency instead of one per slot
-    constexpr int E = sizeof(key) / sizeof(key[0]);
-    uint2 rw[E];
+  const bool want_scores = topk_scores != nullptr;
+
+  // thread 0 keeps the (n, counts) of the row after next in registers: their global
+  // loads are issued one row ahead of use
+  int nx_n = 0, nx_c[kQuadrants] = {0, 0, 0, 0};
+  auto load_meta = [&](int row) {
+    if (row < n_rows) {
+      nx_n = prefix_len[row];
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int e = v3_elem<NT, E>(r);
-      const int q = (e >= off[1]) + (e >= off[2]) + (e >= off[3]);
-      const int64_t at = e < total ? (int64_t)q * cap + (e - off[q]) : 0;
-      rw[r] = __ldcs(reinterpret_cast<const uint2*>(rowc + at));
-    }
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int e = v3_elem<NT, E>(r);
-      if (e < total) si[e] = static_cast<int32_t>(rw[r].y);
-      key[r] = e < total ? float_key(__uint_as_float(rw[r].x)) : 0u;
+      for (int q = 0; q < kQuadrants; ++q) nx_c[q] = cand_count[(int64_t)row * kQuadrants + q];
     }
   };
-  if (kk <= 0) {
-    for (int i = threadIdx.x; i < k; i += NT) {
+  auto issue = [&](int row) {  // thread 0: start the copy of `row` (meta in nx_*)
+    pf.row = row;
+    pf.copy = false;
+    if (row >= n_rows) return;
+    pf.n = nx_n;
+#pragma unroll
+    for (int q = 0; q < kQuadrants; ++q) pf.c[q] = nx_c[q];
+    if (nx_n <= k && !want_scores) return;  // every prefix token; counts unused (may be unset)
+    pf.copy = true;
+    if (!PF) return;
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int q = 0; q < kQuadrants; ++q) bytes += ((min(max(nx_c[q], 0), cap) * 8u) + 15u) & ~15u;
+    ptx::mbar_arrive_expect_tx(&mbar, bytes);
+#pragma unroll
+    for (int q = 0; q < kQuadrants; ++q) {
+      const uint32_t b = ((min(max(nx_c[q], 0), cap) * 8u) + 15u) & ~15u;
+      if (b) ptx::bulk_g2s(raw + (size_t)q * cap, cand + ((int64_t)row * kQuadrants + q) * cap, b, &mbar);
+    }
+    pf.copy = true;
+  };
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&mbar, 1);
+    ptx::fence_mbar_init();
+    load_meta(blockIdx.x);
+    issue(blockIdx.x);
+    load_meta(blockIdx.x + gridDim.x);
+  }
+  uint32_t phase = 0;
+  for (int t = blockIdx.x; t < n_rows; t += gridDim.x) {
+    __syncthreads();  // pf (row t) visible; the previous row is done with raw / sidx / cidx
+    const int n = pf.n;
+    const bool copy = pf.copy;
+    int c[kQuadrants];
+#pragma unroll
+    for (int q = 0; q < kQuadrants; ++q) c[q] = pf.c[q];
+    int32_t* out = topk + (int64_t)t * topk_ld;
+    float* outs = want_scores ? topk_scores + (int64_t)t * topk_ld : nullptr;
+    const int kk = n < k ? n : k;
+    if (!copy) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73)
+      __syncthreads();  // everyone has read pf before it is overwritten
+      if (threadIdx.x == 0) {
+        issue(t + gridDim.x);
+        load_meta(t + 2 * gridDim.x);
+      }
+      for (int i = threadIdx.x; i < k; i += NT) out[i] = i < n ? i : -1;
+      if (threadIdx.x == 0 && flags) flags[t] = 0;
+      continue;
+    }
+    int off[kQuadrants + 1];
+    bool overflow = false;
+    off[0] = 0;
+#pragma unroll
+    for (int q = 0; q < kQuadrants; ++q) {
+      overflow |= c[q] > cap;
+      off[q + 1] = off[q] + min(max(c[q], 0), cap);
+    }
+    const int total = off[kQuadrants];
+    if (PF) {
+      ptx::mbar_wait(&mbar, phase);
+      phase ^= 1;
+    }
+    const bool bad = overflow || total < kk || total > NT * EPT;
+    uint32_t key[EPT];
+    if (!bad) {
+      // PF: from the staged copy; else straight from global with every load issued
+      // before its first use (one memory latency per row)
+      const uint64_t* src = PF ? raw : cand + (int64_t)t * kQuadrants * cap;
+      uint2 rw[EPT];
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const int e = v3_elem<NT, EPT>(r);
+        const int q = (e >= off[1]) + (e >= off[2]) + (e >= off[3]);
+        const uint2* at = reinterpret_cast<const uint2*>(src + (e < total ? (size_t)q * cap + (e - off[q]) : 0));
+        rw[r] = PF ? *at : __ldcs(at);
+      }
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const int e = v3_elem<NT, EPT>(r);
+        if (e < total) sidx[e] = static_cast<int32_t>(rw[r].y);
+        key[r] = e < total ? float_key(__uint_as_float(rw[r].x)) : 0u;
+      }
+    }
+    if (threadIdx.x <= kQuadrants) sh.lst_off[threadIdx.x] = off[threadIdx.x];
+    __syncthreads();  // raw consumed, sidx / lst_off staged
+    if (threadIdx.x == 0) {
+      issue(t + gridDim.x);
+      load_meta(t + 2 * gridDim.x);
+    }
+    if (bad) {
+      for (int i = threadIdx.x; i < k; i += NT) out[i] = -1;
+      if (threadIdx.x == 0 && flags)
+        flags[t] = (overflow || total > NT * EPT) ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
+      continue;
+    }
+    if (kk <= 0) {
+      for (int i = threadIdx.x; i < k; i += NT) {
+        out[i] = -1;
+        if (outs) outs[i] = -INFINITY;
+      }
+    } else {
+      v3_select<NT, EPT>(key, sidx, total, kQuadrants, kk, sh, cidx, outs ? csc : nullptr, out, outs, k);
+    }
+    if (threadIdx.x == 0 && flags) flags[t] = 0;
+  }
+}
+
+// ---------------------------------------------- v5 candidates -> top-k ----
+// Persistent, prefetching, merge-free.  Warp w owns slots of quadrant list
+// q = w / (NW/4) (NT*EPT == 4*cap, cap a multiple of 32*EPT), so extraction is one
+// shared load per slot and the compaction order is list-major.  The ascending output
+// needs no merge: the scorer's quadrant q holds exactly the 32-key chunks c = idx/32
+// with c % 4 == q, so all selected elements of a chunk are contiguous in one list and
+//   pos = #selected in chunks < c (block scan of a chunk histogram) + rank within c.
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict__ cand,
+                                                      const int32_t* __restrict__ cand_count, int cap,
+                                                      const int32_t* __restrict__ prefix_len, int n_rows, int k,
+                                                      int n_chunks, int32_t* __restrict__ topk, int64_t topk_ld,
+                                                      float* __restrict__ topk_scores, int32_t* __restrict__ flags) {
+  constexpr int NW = NT / 32, WPL = NW / kQuadrants, WE = 32 * EPT;
+  static_assert(NW % kQuadrants == 0, "warps split evenly over the quadrant lists");
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ SelSh<NT> sh;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ TopkPrefetch pf;
+  uint64_t* raw = reinterpret_cast<uint64_t*>(dsm);                    // list q at raw + q*cap
+  uint32_t* H = reinterpret_cast<uint32_t*>(raw + (size_t)kQuadrants * cap);  // chunk counts -> prefix
+  uint16_t* G0 = reinterpret_cast<uint16_t*>(H + n_chunks);             // first compacted rank of a chunk
+  int32_t* cidx = reinterpret_cast<int32_t*>(G0 + ((n_chunks + 7) & ~7));  // compacted indices
+  const bool want_scores = topk_scores != nullptr;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int q = w / WPL;                       // this warp's quadrant list
+  const int i0 = (w % WPL) * WE + lane;        // list position of slot 0 (slot r: i0 + 32r)
+
+  int nx_n = 0, nx_c[kQuadrants] = {0, 0, 0, 0};
+  auto load_meta = [&](int row) {
+    if (row < n_rows) {
+      nx_n = prefix_len[row];
+#pragma unroll
+      for (int j = 0; j < kQuadrants; ++j) nx_c[j] = cand_count[(int64_t)row * kQuadrants + j];
+    }
+  };
+  auto issue = [&](int row) {
+    pf.row = row;
+    pf.copy = false;
+    if (row >= n_rows) return;
+    pf.n = nx_n;
+#pragma unroll
+    for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nx_c[j];
+    if (nx_n <= k && !want_scores) return;
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int j = 0; j < kQuadrants; ++j) bytes += ((min(max(nx_c[j], 0), cap) * 8u) + 15u) & ~15u;
+    ptx::mbar_arrive_expect_tx(&mbar, bytes);
+#pragma unroll
+    for (int j = 0; j < kQuadrants; ++j) {
+      const uint32_t b = ((min(max(nx_c[j], 0), cap) * 8u) + 15u) & ~15u;
+      if (b) ptx::bulk_g2s(raw + (size_t)j * cap, cand + ((int64_t)row * kQuadrants + j) * cap, b, &mbar);
+    }
+    pf.copy = true;
+  };
+  if (tid == 0) {
+    ptx::mbar_init(&mbar, 1);
+    ptx::fence_mbar_init();
+    load_meta(blockIdx.x);
+    issue(blockIdx.x);
+    load_meta(blockIdx.x + gridDim.x);
+  }
+  uint32_t phase = 0;
+  for (int t = blockIdx.x; t < n_rows; t += gridDim.x) {
+    __syncthreads();
+    const int n = pf.n;
+    const bool copy = pf.copy;
+    int c[kQuadrants];
+#pragma unroll
+    for (int j = 0; j < kQuadrants; ++j) c[j] = pf.c[j];
+    int32_t* out = topk + (int64_t)t * topk_ld;
+    float* outs = want_scores ? topk_scores + (int64_t)t * topk_ld : nullptr;
+    const int kk = n < k ? n : k;
+    if (!copy) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73)
+      __syncthreads();
+      if (tid == 0) {
+        issue(t + gridDim.x);
+        load_meta(t + 2 * gridDim.x);
+      }
+      for (int i = tid; i < k; i += NT) out[i] = i < n ? i : -1;
+      if (tid == 0 && flags) flags[t] = 0;
+      continue;
+    }
+    bool overflow = false;
+    int total = 0;
+#pragma unroll
+    for (int j = 0; j < kQuadrants; ++j) {
+      overflow |= c[j] > cap;
+      total += min(max(c[j], 0), cap);
+    }
+    const int cq = min(max(c[q], 0), cap);
+    ptx::mbar_wait(&mbar, phase);
+    phase ^= 1;
+    uint32_t key[EPT];
+    int32_t idx[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const int i = i0 + 32 * r;
+      const uint2 rw = *reinterpret_cast<const uint2*>(raw + (size_t)q * cap + (i < cq ? i : 0));
+      key[r] = i < cq ? float_key(__uint_as_float(rw.x)) : 0u;
+      idx[r] = static_cast<int32_t>(rw.y);
+    }
+    __syncthreads();  // raw consumed: start the next row's copy
+    if (tid == 0) {
+      issue(t + gridDim.x);
+      load_meta(t + 2 * gridDim.x);
+    }
+    if (overflow || total < kk) {
+      for (int i = tid; i < k; i += NT) out[i] = -1;
+      if (tid == 0 && flags) flags[t] = overflow ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
+      continue;
+    }
+    // ---- cut: kk-th element under (score desc, index asc)
+    uint32_t v = 0;
+    int thr = 0x7fffffff;
+    int parity = 0;
+    if (kk < total) hist_cut<NT, EPT>(key, [&](int r) { return idx[r]; }, total, kk, sh, parity, v, thr);
+    // ---- compaction (list-major slot order)
+    const int nch = (n + 31) >> 5;
+    uint32_t selm = 0;
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      bool sel = key[r] != 0u;
+      if (kk < total) sel = sel && (key[r] > v || (key[r] == v && idx[r] <= thr));
+      const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+      selm |= (sel ? 1u : 0u) << r;
+      cnt += __popc(bal);
+    }
+    if (lane == 0) sh.wtot[w] = cnt;
+    for (int i = tid; i < nch; i += NT) H[i] = 0u;
+    __syncthreads();
+    int run = 0;
+    for (int i = 0; i < w; ++i) run += sh.wtot[i];
+    if (lane == 0 && w % WPL == 0) sh.lst_g[q] = run;
+    const uint32_t lt = ptx::lanemask_lt();
+    int g[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (selm >> r) & 1u);
+      g[r] = run + __popc(bal & lt);
+      if ((selm >> r) & 1u) cidx[g[r]] = idx[r];
+      run += __popc(bal);
+    }
+    __syncthreads();
+    // ---- chunk segments: the first selected element of each chunk records its rank
+    const int gq = sh.lst_g[q];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      if ((selm >> r) & 1u) {
+        const int ch = idx[r] >> 5;
+        const bool start = g[r] == gq || (cidx[g[r] - 1] >> 5) != ch;
+        if (start) G0[ch] = static_cast<uint16_t>(g[r]);
+        atomicAdd(&H[ch], 1u);
+      }
+    }
+    __syncthreads();
+    // ---- exclusive scan of the chunk histogram (in place)
+    {
+      const int per = (nch + NT - 1) / NT;
+      const int c0 = min(nch, tid * per), c1 = min(nch, c0 + per);
+      int s = 0;
+      for (int i = c0; i < c1; ++i) s += static_cast<int>(H[i]);
+      int incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) sh.hscan[w] = incl;
+      __syncthreads();
+      int base = incl - s;
+      for (int i = 0; i < w; ++i) base += sh.hscan[i];
+      for (int i = c0; i < c1; ++i) {
+        const int h = static_cast<int>(H[i]);
+        H[i] = static_cast<uint32_t>(base);
+        base += h;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      if ((selm >> r) & 1u) {
+        const int ch = idx[r] >> 5;
+        const int pos = static_cast<int>(H[ch]) + g[r] - static_cast<int>(G0[ch]);
+        out[pos] = idx[r];
+        if (outs) outs[pos] = key_float(key[r]);
+      }
+    }
+    for (int i = kk + tid; i < k; i += NT) {
       out[i] = -1;
       if (outs) outs[i] = -INFINITY;
     }
-  } else {
-    v3_dispatch<NT, EPT>(total, load, kQuadrants, kk, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
+    if (tid == 0 && flags) flags[t] = 0;
   }
-  if (threadIdx.x == 0 && flags) flags[t] = 0;
 }
 
 // ------------------------------------------------------- dense rows ----
@@ -990,9 +1259,21 @@ template <int NT, int EPT>
 struct TopkL {
   static int go(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl, int64_t T,
                 int k, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
-    const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 16;
-    MISA_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    topk_kernel<NT, EPT><<<(unsigned)T, NT, bytes, st>>>(cand, cc, cap, pl, k, topk, ld, ts, flags);
+    const size_t base = (size_t)NT * EPT * 4 + (size_t)k * (ts ? 16 : 8);
+    const size_t staged = base + (size_t)kQuadrants * cap * 8;
+    if (staged <= 110 * 1024) return run<true>(st, staged, cand, cc, cap, pl, T, k, topk, ld, ts, flags);
+    MISA_REQUIRE(base <= 200 * 1024, "selector working set %zu B exceeds shared memory (k %d)", base, k);
+    return run<false>(st, base, cand, cc, cap, pl, T, k, topk, ld, ts, flags);
+  }
+  template <bool PF>
+  static int run(cudaStream_t st, size_t bytes, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl,
+                 int64_t T, int k, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
+    auto kern = topk_kernel<NT, EPT, PF>;
+    MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    int per_sm = 0;
+    MISA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes));
+    const int64_t grid = std::min<int64_t>(T, (int64_t)sm_count() * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, NT, bytes, st>>>(cand, cc, cap, pl, (int)T, k, topk, ld, ts, flags);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
   }
@@ -1023,6 +1304,35 @@ struct MergeL {
     return MISA_OK;
   }
 };
+// v5 selector when the quadrant capacity maps onto whole warps and the staging fits.
+template <int NT, int EPT>
+static int launch_topk5_t(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl,
+                          int64_t T, int k, int n_chunks, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
+  const size_t bytes = (size_t)kQuadrants * cap * 8 + (size_t)n_chunks * 4 + (((size_t)n_chunks + 7) & ~size_t(7)) * 2 +
+                       (size_t)(k + kBucketMax) * 4;
+  if (bytes > 110 * 1024) return -100;
+  auto kern = topk5_kernel<NT, EPT>;
+  MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  int per_sm = 0;
+  MISA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes));
+  const int64_t grid = std::min<int64_t>(T, (int64_t)sm_count() * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, NT, bytes, st>>>(cand, cc, cap, pl, (int)T, k, n_chunks, topk, ld, ts, flags);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}
+
+static int launch_topk5(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl,
+                        int64_t T, int k, int64_t max_n, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
+  const int64_t n_chunks = (max_n + 31) / 32;
+  if (n_chunks > 8192 || cap > 0xffff) return -100;
+  const int nc = static_cast<int>(n_chunks);
+  // NT*EPT == 4*cap with cap a multiple of 32*EPT*(NT/128)
+  if (cap == 256 * 8 / 4) return launch_topk5_t<256, 8>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+  if (cap == 256 * 16 / 4) return launch_topk5_t<256, 16>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+  if (cap == 256 * 24 / 4) return launch_topk5_t<256, 24>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+  if (cap == 256 * 32 / 4) return launch_topk5_t<256, 32>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+  return -100;
+}
 }  // namespace
 
 extern "C" int misa_select_threshold(const float* sample_scores, int64_t ld, const int32_t* prefix_len,
@@ -1037,12 +1347,17 @@ extern "C" int misa_select_threshold(const float* sample_scores, int64_t ld, con
 }
 
 extern "C" int misa_select_topk(const uint64_t* cand, const int32_t* cand_count, int cap, const int32_t* prefix_len,
-                                int64_t n_rows, int k, int32_t* topk, int64_t topk_ld, float* topk_scores,
-                                int32_t* flags, void* stream) {
+                                int64_t n_rows, int k, int64_t max_prefix_len, int32_t* topk, int64_t topk_ld,
+                                float* topk_scores, int32_t* flags, void* stream) {
   MISA_REQUIRE(cand && cand_count && prefix_len && topk, "null pointer");
   MISA_REQUIRE(k >= 1 && cap >= 1 && topk_ld >= k && n_rows >= 1, "bad top-k arguments");
   MISA_REQUIRE((int64_t)kQuadrants * cap <= 512 * 32, "candidate capacity %d exceeds the register selector", cap);
   MISA_REQUIRE((size_t)k * 16 <= 200 * 1024, "k too large");
+  if (max_prefix_len > 0) {
+    const int rc = launch_topk5(as_stream(stream), cand, cand_count, cap, prefix_len, n_rows, k, max_prefix_len, topk,
+                                topk_ld, topk_scores, flags);
+    if (rc != -100) return rc;
+  }
   return dispatch_capacity<TopkL>((int64_t)kQuadrants * cap, as_stream(stream), cand, cand_count, cap, prefix_len,
                                   n_rows, k, topk, topk_ld, topk_scores, flags);
 }

@@ -242,7 +242,10 @@ def test_threshold_and_filter_select_roundtrip():
              items.numel(), _p(tau), _p(cand), cap, _p(cnt), _stream())
     topk = torch.empty(T, k, dtype=torch.int32, device="cuda")
     flags = torch.empty(T, dtype=torch.int32, device="cuda")
-    lib.call("misa_select_topk", _p(cand), _p(cnt), cap, _p(prefix), T, k, _p(topk), k, None, _p(flags), _stream())
+    lib.call("misa_select_topk", _p(cand), _p(cnt), cap, _p(prefix), T, k, L, _p(topk), k, None, _p(flags), _stream())
+    # the pre-v5 path (unknown max prefix) gives the same rows
+    topk_v3 = torch.empty_like(topk)
+    lib.call("misa_select_topk", _p(cand), _p(cnt), cap, _p(prefix), T, k, 0, _p(topk_v3), k, None, None, _stream())
     # dense reference through the same scoring kernel + dense select
     full = torch.empty(T, L, device="cuda")
     lib.call("misa_score_materialize", _p(K), L, 1, D, _p(Q), _p(W), H, H, None, 64, _p(prefix), T, _p(items),
@@ -252,6 +255,7 @@ def test_threshold_and_filter_select_roundtrip():
     torch.cuda.synchronize()
     assert (flags == 0).all(), flags.nonzero()
     assert torch.equal(topk, ref)
+    assert torch.equal(topk_v3, ref)
     # candidates are never more than a few x k
     tot = cnt.view(T, 4).sum(1)
     big = prefix > 4 * cap

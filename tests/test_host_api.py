@@ -28,12 +28,12 @@ def test_abi_library_exports_every_header_symbol():
     for n in names:
         assert hasattr(lib, n), n
         assert n in _lib.SIGNATURES or n in _lib.EXTRA, f"{n} not typed in _lib"
-    assert lib.misa_abi_version() == 1
+    assert lib.misa_abi_version() == 2
     # argument validation happens before any device work: a bad shape is EINVAL -> ValueError
     with pytest.raises(ValueError):
         _lib.call("misa_pool_keys", None, 10, 128, 4, None, None, None, 0, None)
     with pytest.raises(ValueError):
-        _lib.call("misa_select_topk", None, None, 4, None, 1, 8, None, 8, None, None, None)
+        _lib.call("misa_select_topk", None, None, 4, None, 1, 8, 0, None, 8, None, None, None)
 
 
 def test_sass_contains_tcgen05_and_tma():
