@@ -414,7 +414,9 @@ __device__ void v3_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N, i
 // ranked exactly by (key desc, index asc) with one element per thread.
 template <int NT, int EPT, typename IdxFn>
 __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk, SelSh<NT>& sh, int& parity,
-                         uint32_t& v_out, int& thr_out) {
+                         uint32_t& v_out, int& thr_out, int rv = EPT) {
+  // rv: warp-uniform number of leading slot rows that can hold valid keys (rows >= rv
+  // are skipped without issuing their instructions)
   constexpr int NW = NT / 32;
   constexpr int NB = 2048, BPT = NB / NT;  // bins per thread
   static_assert(NB % NT == 0 && BPT >= 1 && BPT <= 16, "bins per thread");
@@ -422,7 +424,7 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
   uint32_t mn = 0xffffffffu, mx = 0u;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    if (key[r]) {
+    if (r < rv && key[r]) {
       mn = min(mn, key[r]);
       mx = max(mx, key[r]);
     }
@@ -450,8 +452,10 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
   for (;;) {
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      const uint32_t d = key[r] - lo;
-      if (key[r] && d <= span_m1) atomicAdd(&sh.hist[d >> sft], 1u);
+      if (r < rv) {
+        const uint32_t d = key[r] - lo;
+        if (key[r] && d <= span_m1) atomicAdd(&sh.hist[d >> sft], 1u);
+      }
     }
     __syncthreads();
     // thread tid owns bins [NB - BPT*(tid+1), NB - BPT*tid): descending key order
@@ -499,7 +503,7 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
   if (cB <= kBucketMax) {
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      if (key[r] && key[r] - lo <= span_m1) {
+      if (r < rv && key[r] && key[r] - lo <= span_m1) {
         const int p = atomicAdd(&sh.bcount, 1);
         sh.bkey[p] = key[r];
         sh.bidx[p] = idx_of(r);
@@ -667,7 +671,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uin
                                                   const int32_t* __restrict__ prefix_len, int n_rows, int k,
                                                   int32_t* __restrict__ topk, int64_t topk_ld,
                                                   float* __restrict__ topk_scores, int32_t* __restrict__ flags) {
-  extern __shared__ __align__(128) uint8_t dsm[];
+  extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ SelSh<NT> sh;
   __shared__ __align__(8) uint64_t mbar;
   __shared__ TopkPrefetch pf;
@@ -794,6 +798,20 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uin
   }
 }
 
+// Optional phase trace (tools/sel_trace: built with -DMISA_SEL_TRACE, never in the product).
+#ifdef MISA_SEL_TRACE
+__device__ unsigned long long g_sel_trace[64][16];
+#define SEL_MARK(row_i, ph)                                                   \
+  do {                                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (row_i) < 64) g_sel_trace[row_i][ph] = clock64(); \
+  } while (0)
+#else
+#define SEL_MARK(row_i, ph) \
+  do {                      \
+  } while (0)
+#endif
+
+
 // ---------------------------------------------- v5 candidates -> top-k ----
 // Persistent, prefetching, merge-free.  Warp w owns slots of quadrant list
 // q = w / (NW/4) (NT*EPT == 4*cap, cap a multiple of 32*EPT), so extraction is one
@@ -809,7 +827,7 @@ __global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict
                                                       float* __restrict__ topk_scores, int32_t* __restrict__ flags) {
   constexpr int NW = NT / 32, WPL = NW / kQuadrants, WE = 32 * EPT;
   static_assert(NW % kQuadrants == 0, "warps split evenly over the quadrant lists");
-  extern __shared__ __align__(128) uint8_t dsm[];
+  extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ SelSh<NT> sh;
   __shared__ __align__(8) uint64_t mbar;
   __shared__ TopkPrefetch pf;
@@ -817,6 +835,7 @@ __global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict
   uint32_t* H = reinterpret_cast<uint32_t*>(raw + (size_t)kQuadrants * cap);  // chunk counts -> prefix
   uint16_t* G0 = reinterpret_cast<uint16_t*>(H + n_chunks);             // first compacted rank of a chunk
   int32_t* cidx = reinterpret_cast<int32_t*>(G0 + ((n_chunks + 7) & ~7));  // compacted indices
+  float* csc = reinterpret_cast<float*>(cidx + k);                       // compacted scores (optional)
   const bool want_scores = topk_scores != nullptr;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int q = w / WPL;                       // this warp's quadrant list
@@ -859,6 +878,8 @@ __global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < n_rows; t += gridDim.x) {
     __syncthreads();
+    const int ti_ = (t - blockIdx.x) / gridDim.x;
+    SEL_MARK(ti_, 0);
     const int n = pf.n;
     const bool copy = pf.copy;
     int c[kQuadrants];
@@ -885,18 +906,26 @@ __global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict
       total += min(max(c[j], 0), cap);
     }
     const int cq = min(max(c[q], 0), cap);
+    // slot rows of this warp that can hold list elements (warp-uniform)
+    const int rv = min(EPT, max(0, (cq - (w % WPL) * WE + 31) >> 5));
     ptx::mbar_wait(&mbar, phase);
     phase ^= 1;
+    SEL_MARK(ti_, 1);
     uint32_t key[EPT];
     int32_t idx[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      const int i = i0 + 32 * r;
-      const uint2 rw = *reinterpret_cast<const uint2*>(raw + (size_t)q * cap + (i < cq ? i : 0));
-      key[r] = i < cq ? float_key(__uint_as_float(rw.x)) : 0u;
-      idx[r] = static_cast<int32_t>(rw.y);
+      key[r] = 0u;
+      idx[r] = 0;
+      if (r < rv) {
+        const int i = i0 + 32 * r;
+        const uint2 rw = *reinterpret_cast<const uint2*>(raw + (size_t)q * cap + (i < cq ? i : 0));
+        key[r] = i < cq ? float_key(__uint_as_float(rw.x)) : 0u;
+        idx[r] = static_cast<int32_t>(rw.y);
+      }
     }
     __syncthreads();  // raw consumed: start the next row's copy
+    SEL_MARK(ti_, 2);
     if (tid == 0) {
       issue(t + gridDim.x);
       load_meta(t + 2 * gridDim.x);
@@ -910,47 +939,53 @@ __global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict
     uint32_t v = 0;
     int thr = 0x7fffffff;
     int parity = 0;
-    if (kk < total) hist_cut<NT, EPT>(key, [&](int r) { return idx[r]; }, total, kk, sh, parity, v, thr);
-    // ---- compaction (list-major slot order)
+    if (kk < total) hist_cut<NT, EPT>(key, [&](int r) { return idx[r]; }, total, kk, sh, parity, v, thr, rv);
+    SEL_MARK(ti_, 3);
+    // ---- compaction of the selected elements (list-major order) into cidx / csc
     const int nch = (n + 31) >> 5;
     uint32_t selm = 0;
     int cnt = 0;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      bool sel = key[r] != 0u;
-      if (kk < total) sel = sel && (key[r] > v || (key[r] == v && idx[r] <= thr));
-      const uint32_t bal = __ballot_sync(0xffffffffu, sel);
-      selm |= (sel ? 1u : 0u) << r;
-      cnt += __popc(bal);
+      if (r < rv) {
+        bool sel = key[r] != 0u;
+        if (kk < total) sel = sel && (key[r] > v || (key[r] == v && idx[r] <= thr));
+        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+        selm |= (sel ? 1u : 0u) << r;
+        cnt += __popc(bal);
+      }
     }
     if (lane == 0) sh.wtot[w] = cnt;
     for (int i = tid; i < nch; i += NT) H[i] = 0u;
     __syncthreads();
+    SEL_MARK(ti_, 4);
     int run = 0;
     for (int i = 0; i < w; ++i) run += sh.wtot[i];
-    if (lane == 0 && w % WPL == 0) sh.lst_g[q] = run;
     const uint32_t lt = ptx::lanemask_lt();
-    int g[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (selm >> r) & 1u);
-      g[r] = run + __popc(bal & lt);
-      if ((selm >> r) & 1u) cidx[g[r]] = idx[r];
-      run += __popc(bal);
-    }
-    __syncthreads();
-    // ---- chunk segments: the first selected element of each chunk records its rank
-    const int gq = sh.lst_g[q];
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) {
-      if ((selm >> r) & 1u) {
-        const int ch = idx[r] >> 5;
-        const bool start = g[r] == gq || (cidx[g[r] - 1] >> 5) != ch;
-        if (start) G0[ch] = static_cast<uint16_t>(g[r]);
-        atomicAdd(&H[ch], 1u);
+      if (r < rv) {
+        const bool sel = (selm >> r) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+        if (sel) {
+          const int g = run + __popc(bal & lt);
+          cidx[g] = idx[r];
+          if (want_scores) csc[g] = key_float(key[r]);
+        }
+        run += __popc(bal);
       }
     }
     __syncthreads();
+    SEL_MARK(ti_, 5);
+    // ---- chunk segments over the compacted elements (dense: no predicated slots);
+    // a chunk's elements are contiguous, its first one records its rank
+    for (int g = tid; g < kk; g += NT) {
+      const int ch = cidx[g] >> 5;
+      if (g == 0 || (cidx[g - 1] >> 5) != ch) G0[ch] = static_cast<uint16_t>(g);
+      atomicAdd(&H[ch], 1u);
+    }
+    __syncthreads();
+    SEL_MARK(ti_, 6);
     // ---- exclusive scan of the chunk histogram (in place)
     {
       const int per = (nch + NT - 1) / NT;
@@ -974,22 +1009,28 @@ __global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) {
-      if ((selm >> r) & 1u) {
-        const int ch = idx[r] >> 5;
-        const int pos = static_cast<int>(H[ch]) + g[r] - static_cast<int>(G0[ch]);
-        out[pos] = idx[r];
-        if (outs) outs[pos] = key_float(key[r]);
-      }
+    SEL_MARK(ti_, 7);
+    for (int g = tid; g < kk; g += NT) {
+      const int x = cidx[g];
+      const int ch = x >> 5;
+      const int pos = static_cast<int>(H[ch]) + g - static_cast<int>(G0[ch]);
+      out[pos] = x;
+      if (want_scores) outs[pos] = csc[g];
     }
     for (int i = kk + tid; i < k; i += NT) {
       out[i] = -1;
       if (outs) outs[i] = -INFINITY;
     }
+    SEL_MARK(ti_, 8);
     if (tid == 0 && flags) flags[t] = 0;
   }
 }
+
+#ifdef MISA_SEL_TRACE
+extern "C" int misa_debug_sel_trace(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_sel_trace, sizeof(g_sel_trace)) == cudaSuccess ? 0 : -2;
+}
+#endif
 
 // ------------------------------------------------------- dense rows ----
 template <int NT, int EPT>
@@ -1309,7 +1350,7 @@ template <int NT, int EPT>
 static int launch_topk5_t(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl,
                           int64_t T, int k, int n_chunks, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
   const size_t bytes = (size_t)kQuadrants * cap * 8 + (size_t)n_chunks * 4 + (((size_t)n_chunks + 7) & ~size_t(7)) * 2 +
-                       (size_t)(k + kBucketMax) * 4;
+                       (size_t)k * (ts ? 8 : 4);
   if (bytes > 110 * 1024) return -100;
   auto kern = topk5_kernel<NT, EPT>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -1354,8 +1395,8 @@ extern "C" int misa_select_topk(const uint64_t* cand, const int32_t* cand_count,
   MISA_REQUIRE((int64_t)kQuadrants * cap <= 512 * 32, "candidate capacity %d exceeds the register selector", cap);
   MISA_REQUIRE((size_t)k * 16 <= 200 * 1024, "k too large");
   if (max_prefix_len > 0) {
-    const int rc = launch_topk5(as_stream(stream), cand, cand_count, cap, prefix_len, n_rows, k, max_prefix_len, topk,
-                                topk_ld, topk_scores, flags);
+    const int rc = launch_topk5(as_stream(stream), cand, cand_count, cap, prefix_len, n_rows, k, max_prefix_len, topk, topk_ld,
+                      topk_scores, flags);
     if (rc != -100) return rc;
   }
   return dispatch_capacity<TopkL>((int64_t)kQuadrants * cap, as_stream(stream), cand, cand_count, cap, prefix_len,

@@ -320,7 +320,8 @@ class IndexerEngine:
                       _ptr(cand), cap, _ptr(cnt), stream)
         flags = self._buf(tag + "_flags", (x.T,), torch.int32, dev)
         self._mark(tag + ":select")
-        _lib.call("misa_select_topk", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, x.L, _ptr(out), out.stride(0),
+        _lib.call("misa_select_topk", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, x.L, _ptr(out),
+                  out.stride(0),
                   _ptr(scores), _ptr(flags), stream)
         self._mark(tag + ":end")
         if not self.check_overflow:
