@@ -2,15 +2,19 @@
 //
 // Row t re-scores its k' coarse candidates with ALL H heads:
 //   out[t][i] = sum_j w_{t,j} ReLU(q_{t,j} . k_{cand[t][i]})
-// The A operand is a gather of candidate key rows: four producer warps (one
-// thread per tile row) copy each row with 16-byte cp.async straight into the
-// 128-B-swizzled K-major layout the UMMA descriptor expects, LAG tiles in flight
-// per thread (cp.async.wait_group), then fence the generic->async proxy and
-// arrive on the stage's mbarrier.  B is the row's Hp query heads (padded to
-// N >= 16), resident in smem for the row's tiles.  The contraction is
-// L2-bandwidth bound (the whole key set stays L2-resident: 32 MiB at 128K).
+// The A operand is a gather of candidate key rows: four producer warps copy them
+// with 16-byte cp.async, half a warp per key row so every warp instruction moves two
+// whole rows (coalesced, no partial sectors), straight into the 128-B-swizzled K-major
+// layout the UMMA descriptor expects; completion is tracked by the stage mbarrier
+// (cp.async.mbarrier.arrive.noinc), candidate indices are prefetched tiles ahead.
+// (TMA tile::gather4 was measured slower here: its per-SM issue rate, not L2, bounds
+// 4-row gathers.)  B = the row's Hp query heads and gate weights, TMA-loaded into one
+// of two buffers so the next row's operands land while this row computes.  The
+// contraction is L2-bandwidth bound (the key set stays L2-resident: 32 MiB at 128K);
+// the epilogue runs four warp sets over a 4-deep TMEM accumulator ring.
 //
-// Warps: 0-3 producers, 4-7 epilogue (TMEM lane quadrants 0-3), 8 MMA issuer.
+// Warps: 0-3 producers (+ B loads), 4 MMA issuer, 5..20 epilogue (set = tile % 4,
+// TMEM lane quadrant = warp % 4).
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -18,16 +22,43 @@ namespace misa {
 
 struct RefineArgs {
   const __nv_bfloat16* __restrict__ keys;  // [n_keys][D]
-  const __nv_bfloat16* __restrict__ q;
   const float* __restrict__ w;
   const int32_t* __restrict__ cand;
   int64_t cand_ld;
   const int32_t* __restrict__ n_cand;
   const int32_t* __restrict__ items;  // rows, longest first
   int n_items;
+  int n_keys;
   int T, H, Hp;
   float* out;
   int64_t out_ld;
+};
+
+constexpr int kRefSets = 4;                              // epilogue warp sets = TMEM accumulators
+constexpr int kRefProd = 4;                              // cp.async producer warps
+constexpr int kRefMma = kRefProd;                        // MMA warp index
+constexpr int kRefEpi0 = kRefProd + 1;                   // first epilogue warp
+constexpr int kRefThreads = 32 * (kRefEpi0 + 4 * kRefSets);  // 672
+
+template <int D, int N>
+struct RefineCfg {
+  static constexpr int STAGES = (D == 128) ? 4 : 6;
+  static constexpr int A_ATOM = 128 * 128;
+  static constexpr int A_BYTES = A_ATOM * (D / 64);
+  static constexpr int B_ATOM = N * 128;
+  static constexpr int B_BYTES = B_ATOM * (D / 64);
+  static constexpr int B_STRIDE = ((B_BYTES + 1023) / 1024) * 1024;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = STAGES * A_BYTES;       // 2 buffers
+  static constexpr int OFF_W = OFF_B + 2 * B_STRIDE;   // 2 x N f32
+  static constexpr int OFF_BAR = OFF_W + 2 * N * 4;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * kRefSets + 4;
+  static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
+  static constexpr int TMEM_COLS = (kRefSets * N <= 32) ? 32 : (kRefSets * N <= 64) ? 64 : (kRefSets * N <= 128) ? 128
+                                   : (kRefSets * N <= 256) ? 256 : 512;
+  static_assert(kRefSets * N <= 512, "TMEM accumulator ring");
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
 
 // 16-byte async global->shared copy; src_bytes = 0 zero-fills the destination.
@@ -36,35 +67,14 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, uin
                "r"(src_bytes)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// Arrive on an mbarrier when all of this thread's prior cp.async copies have landed.
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
 }
 
 template <int D, int N>
-struct RefineCfg {
-  static constexpr int STAGES = (D == 128) ? 5 : 8;
-  static constexpr int A_ATOM = 128 * 128;
-  static constexpr int A_BYTES = A_ATOM * (D / 64);
-  static constexpr int B_ATOM = N * 128;
-  static constexpr int B_BYTES = B_ATOM * (D / 64);
-  static constexpr int OFF_A = 0;
-  static constexpr int OFF_B = STAGES * A_BYTES;
-  static constexpr int OFF_W = OFF_B + ((B_BYTES + 1023) / 1024) * 1024;
-  static constexpr int OFF_BAR = OFF_W + N * 4;
-  static constexpr int NUM_BARS = 2 * STAGES + 5;
-  static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
-  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
-  static constexpr int TMEM_COLS = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : (2 * N <= 128) ? 128 : (2 * N <= 256) ? 256 : 512;
-  static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
-};
-
-constexpr int kRefineThreads = 288;
-constexpr int kLag = 2;  // cp.async tile groups in flight per producer thread
-
-template <int D, int N>
-__global__ void __launch_bounds__(kRefineThreads, 1) refine_kernel(const RefineArgs a) {
+__global__ void __launch_bounds__(kRefThreads, 1)
+    refine_kernel(const __grid_constant__ CUtensorMap tmap_q, const RefineArgs a) {
   using C = RefineCfg<D, N>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -76,25 +86,31 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_kernel(const RefineA
   uint64_t* full_a = bars;
   uint64_t* empty_a = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;
+  uint64_t* tempty = tfull + kRefSets;
+  uint64_t* bfull = tempty + kRefSets;  // [2]
+  uint64_t* bempty = bfull + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = gridDim.x, bid = blockIdx.x;
 
   if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmap_q);
     for (int i = 0; i < STAGES; ++i) {
-      ptx::mbar_init(&full_a[i], 128);
+      ptx::mbar_init(&full_a[i], 32 * kRefProd);  // one cp.async completion arrival per producer thread
       ptx::mbar_init(&empty_a[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kRefSets; ++i) {
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 128);
     }
-    ptx::mbar_init(bfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&bfull[i], 1);
+      ptx::mbar_init(&bempty[i], 1 + 4 * kRefSets);  // MMA commit + every epilogue warp
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 8) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == kRefMma) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) sW[i] = 0.f;  // weights of pad heads (Hp < N)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -102,63 +118,82 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_kernel(const RefineA
 
   auto item_at = [&](int it) { return (it & 1) ? (it + 1) * P - 1 - bid : it * P + bid; };
 
-  if (warp < 4) {
-    // Producers: thread i copies candidate row i of every 128-row tile.
-    const int pt = threadIdx.x;  // 0..127
+  if (warp < kRefProd) {
+    // ---------------------------------------------------------------- producers
+    // warp p covers tile rows [32p, 32p + 32): instruction i moves rows 32p + 2i and
+    // 32p + 2i + 1 (lanes 0-15 / 16-31, one 16-byte chunk each)
+    const int p = warp, half = lane >> 4, ch = lane & 15;
     int s = 0;
     uint32_t ph = 0;
-    int pend[kLag + 1];
-    int npend = 0;
     for (int it = 0;; ++it) {
       const int idx = item_at(it);
       if (idx >= a.n_items) break;
       const int t = a.items[idx];
       const int nc = a.n_cand[t];
-      const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
       const int nt = (nc + 127) / 128;
-      int ki_next = (pt < nc) ? cr[pt] : -1;
-      for (int j = 0; j < nt; ++j) {
-        const int ki = ki_next;
-        if (j + 1 < nt) ki_next = ((j + 1) * 128 + pt < nc) ? cr[(j + 1) * 128 + pt] : -1;
-        ptx::mbar_wait(&empty_a[s], ph ^ 1);
-        uint8_t* dst = sA + s * C::A_BYTES;
-        const __nv_bfloat16* src = a.keys + (int64_t)(ki < 0 ? 0 : ki) * D;
-        const uint32_t nb = ki < 0 ? 0u : 16u;
+      const int b = it & 1;
+      if (p == 0) {
+        // operands of this row: wait until the buffer's previous row is fully consumed.
+        // N = max(16, Hp): rows past Hp belong to the next query row (or are zero-filled
+        // past the end) and meet zero weights, so they contribute exactly 0
+        ptx::mbar_wait(&bempty[b], ((it >> 1) & 1) ^ 1);
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(&bfull[b], C::B_BYTES + a.Hp * 4);
 #pragma unroll
-        for (int ch = 0; ch < D / 8; ++ch) cp_async16(dst + ptx::sw128_offset(pt, ch * 8, C::A_ATOM), src + ch * 8, nb);
-        cp_async_commit();
-        pend[npend++] = s;
-        if (npend > kLag) {
-          cp_async_wait<kLag>();
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&full_a[pend[0]]);
-#pragma unroll
-          for (int u = 0; u < kLag; ++u) pend[u] = pend[u + 1];
-          --npend;
+          for (int at = 0; at < D / 64; ++at)
+            ptx::tma_load_2d(sB + b * C::B_STRIDE + at * C::B_ATOM, &tmap_q, &bfull[b], at * 64, t * a.Hp);
+          ptx::bulk_g2s(sW + b * N, a.w + (int64_t)t * a.Hp, a.Hp * 4, &bfull[b]);
         }
+      }
+      const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
+      // lane holds the index of tile row 32p + lane, kIdxAhead tiles ahead (register ring)
+      constexpr int kIdxAhead = 4;
+      int ring[kIdxAhead];
+#pragma unroll
+      for (int d = 0; d < kIdxAhead; ++d) {
+        const int i = d * 128 + 32 * p + lane;
+        ring[d] = (d < nt && i < nc) ? __ldg(cr + i) : -1;
+      }
+      for (int j = 0; j < nt; ++j) {
+        ptx::mbar_wait(&empty_a[s], ph ^ 1);
+        uint8_t* stage = sA + s * C::A_BYTES;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = 32 * p + 2 * i + half;
+          const int ki = __shfl_sync(0xffffffffu, ring[0], 2 * i + half);
+          const __nv_bfloat16* src = a.keys + (int64_t)(ki < 0 ? 0 : ki) * D + ch * 8;
+          if (ch * 8 < D)
+            cp_async16(stage + ptx::sw128_offset(r, ch * 8, C::A_ATOM), src, ki < 0 ? 0u : 16u);
+        }
+        cp_async_mbar_arrive(&full_a[s]);
+#pragma unroll
+        for (int d = 0; d + 1 < kIdxAhead; ++d) ring[d] = ring[d + 1];
+        const int i = (j + kIdxAhead) * 128 + 32 * p + lane;
+        ring[kIdxAhead - 1] = (j + kIdxAhead < nt && i < nc) ? __ldg(cr + i) : -1;
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
-    cp_async_wait<0>();
-    ptx::fence_proxy_async_smem();
-    for (int u = 0; u < npend; ++u) ptx::mbar_arrive(&full_a[pend[u]]);
-  } else if (warp == 8) {
+  } else if (warp == kRefMma) {
+    // ---------------------------------------------------------------- MMA issuer
     if (ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
-      int s = 0, acc = 0;
-      uint32_t ph = 0, aph = 0;
-      const uint32_t b_base = ptx::smem_u32(sB);
+      int s = 0;
+      uint32_t ph = 0;
+      int g = 0;  // global tile counter (accumulator ring slot g % kRefSets)
       for (int it = 0;; ++it) {
         const int idx = item_at(it);
         if (idx >= a.n_items) break;
         const int t = a.items[idx];
         const int nt = (a.n_cand[t] + 127) / 128;
-        ptx::mbar_wait(bfull, it & 1);
+        const int b = it & 1;
+        ptx::mbar_wait(&bfull[b], (it >> 1) & 1);
         ptx::tc_fence_after();
-        for (int j = 0; j < nt; ++j) {
-          ptx::mbar_wait(&tempty[acc], aph ^ 1);
+        const uint32_t b_base = ptx::smem_u32(sB + b * C::B_STRIDE);
+        for (int j = 0; j < nt; ++j, ++g) {
+          const int acc = g % kRefSets;
+          ptx::mbar_wait(&tempty[acc], ((g / kRefSets) & 1) ^ 1);
           ptx::mbar_wait(&full_a[s], ph);
-          ptx::fence_proxy_async_smem();
+          ptx::fence_proxy_async_smem();  // cp.async (generic-proxy) writes -> tensor-core reads
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
           const uint32_t d_tmem = tmem_base + acc * N;
@@ -172,70 +207,69 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_kernel(const RefineA
           ptx::mma_commit(&empty_a[s]);
           ptx::mma_commit(&tfull[acc]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
-          if (++acc == 2) { acc = 0; aph ^= 1; }
         }
+        ptx::mma_commit(&bempty[b]);  // B buffer reusable once this row's MMAs are done
       }
     }
   } else {
-    const int et = threadIdx.x - 128;
+    // ---------------------------------------------------------------- epilogue
     const int quad = warp & 3;
-    int acc = 0;
-    uint32_t aph = 0;
+    const int set = (warp - kRefEpi0) >> 2;
+    int g = 0;
     for (int it = 0;; ++it) {
       const int idx = item_at(it);
       if (idx >= a.n_items) break;
       const int t = a.items[idx];
       const int nc = a.n_cand[t];
       const int nt = (nc + 127) / 128;
-      constexpr int CH = D / 8;
-      for (int c = et; c < N * CH; c += 128) {
-        const int r = c / CH, ch = c - r * CH;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (r < a.H) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)t * a.Hp + r) * D + ch * 8);
-        *reinterpret_cast<uint4*>(sB + ptx::sw128_offset(r, ch * 8, C::B_ATOM)) = v;
-      }
-      for (int r = et; r < N; r += 128) sW[r] = r < a.H ? a.w[(int64_t)t * a.Hp + r] : 0.f;
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 128);
-      if (et == 0) ptx::mbar_arrive(bfull);
-      for (int j = 0; j < nt; ++j) {
-        ptx::mbar_wait(&tfull[acc], aph);
-        ptx::tc_fence_after();
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * N;
-        // same head order / accumulators as the scorer (ptx.cuh gate_relu4), so an
-        // all-head re-score reproduces the dense DSA score bit for bit
-        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-        const float4* w4 = reinterpret_cast<const float4*>(sW);
-        uint32_t ra[16], rb[16];
-        ptx::tmem_ld_x16(taddr, ra);
-        ptx::tmem_wait_ld_dep16(ra);
+      const int b = it & 1;
+      const int first = (set - g % kRefSets + kRefSets) % kRefSets;  // this set's first tile in the row
+      if (first < nt) {
+        ptx::mbar_wait(&bfull[b], (it >> 1) & 1);
+        const float4* w4 = reinterpret_cast<const float4*>(sW + b * N);
+        for (int j = first; j < nt; j += kRefSets) {
+          const int gg = g + j;
+          ptx::mbar_wait(&tfull[set], (gg / kRefSets) & 1);
+          ptx::tc_fence_after();
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + set * N;
+          // same head order / accumulators as the dense scorer (score.cu reduce16, HQ > 16;
+          // gate_relu4), so an all-head re-score reproduces the dense DSA score bit for bit
+          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+          uint32_t r[N < 32 ? 32 : 32];
 #pragma unroll
-        for (int c = 0; c < N; c += 32) {
-          if (c + 16 < N) ptx::tmem_ld_x16(taddr + c + 16, rb);
+          for (int c = 0; c < N; c += 32) {
+            if constexpr (N >= 32) {
+              ptx::tmem_ld_x32p(taddr + c, r);
+              ptx::tmem_wait_ld_dep32p(r);
+              if (c + 32 >= N) {  // the accumulator can be refilled once the last chunk is in registers
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[set]);
+              }
 #pragma unroll
-          for (int jj = 0; jj < 16; jj += 4) gate_relu4(s0, s1, w4[(c + jj) / 4], ra[jj], ra[jj + 1], ra[jj + 2], ra[jj + 3]);
-          if (c + 16 < N) {
-            ptx::tmem_wait_ld_dep16(rb);
-            if (c + 32 < N) ptx::tmem_ld_x16(taddr + c + 32, ra);
-#pragma unroll
-            for (int jj = 0; jj < 16; jj += 4)
-              gate_relu4(s0, s1, w4[(c + 16 + jj) / 4], rb[jj], rb[jj + 1], rb[jj + 2], rb[jj + 3]);
-            if (c + 32 < N) ptx::tmem_wait_ld_dep16(ra);
+              for (int jj = 0; jj < 32; jj += 4) gate_relu4(s0, s1, w4[(c + jj) / 4], r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
+            }
           }
+          if constexpr (N < 32) {
+            ptx::tmem_ld_x16(taddr, r);
+            ptx::tmem_wait_ld_dep16(r);
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[set]);
+#pragma unroll
+            for (int jj = 0; jj < N; jj += 4) gate_relu4(s0, s1, w4[jj / 4], r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
+          }
+          const float sc = gate_relu_finish(s0, s1);
+          const int i = j * 128 + quad * 32 + lane;
+          if (i < nc) a.out[(int64_t)t * a.out_ld + i] = sc;
         }
-        const float sc = gate_relu_finish(s0, s1);
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
-        const int i = j * 128 + quad * 32 + lane;
-        if (i < nc) a.out[(int64_t)t * a.out_ld + i] = sc;
       }
-      ptx::named_bar_sync(1, 128);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&bempty[b]);  // this warp no longer reads sW[b]
+      g += nt;
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kRefMma) {
     __syncwarp();
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
@@ -243,13 +277,13 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_kernel(const RefineA
 }
 
 template <int D, int N>
-static int launch_refine_t(const RefineArgs& a, cudaStream_t st) {
+static int launch_refine_t(const CUtensorMap& mq, const RefineArgs& a, cudaStream_t st) {
   using C = RefineCfg<D, N>;
   auto kern = refine_kernel<D, N>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
   const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
   if (grid <= 0) return MISA_OK;
-  kern<<<grid, kRefineThreads, C::SMEM_BYTES, st>>>(a);
+  kern<<<grid, kRefThreads, C::SMEM_BYTES, st>>>(mq, a);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }
@@ -268,15 +302,23 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
   MISA_REQUIRE(n_rows >= 1 && n_keys >= 1, "empty input");
   if (n_items == 0) return MISA_OK;
   MISA_REQUIRE((reinterpret_cast<uintptr_t>(keys) & 15) == 0, "keys must be 16-byte aligned");
+  MISA_REQUIRE(n_heads_pad == 8 || n_heads_pad == 16 || n_heads_pad == 32 || n_heads_pad == 64 ||
+                   n_heads_pad == 128, "n_heads_pad must be a power of two in [8, 128]");
+  MISA_REQUIRE((reinterpret_cast<uintptr_t>(queries) & 15) == 0 && (reinterpret_cast<uintptr_t>(weights) & 15) == 0,
+               "queries / weights must be 16-byte aligned");
+  MISA_REQUIRE(n_keys < (int64_t(1) << 31) - 1, "too many keys");
+  CUtensorMap mq;
+  const int rc = make_tmap_bf16_2d(&mq, queries, head_dim, n_rows * n_heads_pad, head_dim, n_heads_pad < 16 ? 16 : n_heads_pad);
+  if (rc) return rc;
   RefineArgs a{};
   a.keys = static_cast<const __nv_bfloat16*>(keys);
-  a.q = static_cast<const __nv_bfloat16*>(queries);
   a.w = weights;
   a.cand = cand;
   a.cand_ld = cand_ld;
   a.n_cand = n_cand;
   a.items = rows;
   a.n_items = n_items;
+  a.n_keys = (int)n_keys;
   a.T = (int)n_rows;
   a.H = n_heads;
   a.Hp = n_heads_pad;
@@ -285,7 +327,7 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
   cudaStream_t st = as_stream(stream);
   const int N = n_heads_pad < 16 ? 16 : n_heads_pad;
 #define MISA_REFINE_CASE(DD, NN) \
-  if (head_dim == DD && N == NN) return launch_refine_t<DD, NN>(a, st);
+  if (head_dim == DD && N == NN) return launch_refine_t<DD, NN>(mq, a, st);
   MISA_REFINE_CASE(128, 16)
   MISA_REFINE_CASE(128, 32)
   MISA_REFINE_CASE(128, 64)
