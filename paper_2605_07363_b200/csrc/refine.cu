@@ -42,12 +42,14 @@ constexpr int kRefThreads = 32 * (kRefEpi0 + 4 * kRefSets);  // 672
 
 template <int D, int N>
 struct RefineCfg {
-  static constexpr int STAGES = (D == 128) ? 4 : 6;
   static constexpr int A_ATOM = 128 * 128;
   static constexpr int A_BYTES = A_ATOM * (D / 64);
   static constexpr int B_ATOM = N * 128;
   static constexpr int B_BYTES = B_ATOM * (D / 64);
   static constexpr int B_STRIDE = ((B_BYTES + 1023) / 1024) * 1024;
+  // as many gather stages as shared memory holds: the gather is latency x bytes-in-flight bound
+  static constexpr int STAGES_FIT = (227 * 1024 - 1024 - 2 * B_STRIDE - 2 * N * 4 - 512) / A_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = STAGES * A_BYTES;       // 2 buffers
   static constexpr int OFF_W = OFF_B + 2 * B_STRIDE;   // 2 x N f32

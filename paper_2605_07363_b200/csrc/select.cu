@@ -820,7 +820,7 @@ __device__ unsigned long long g_sel_trace[64][16];
 // with c % 4 == q, so all selected elements of a chunk are contiguous in one list and
 //   pos = #selected in chunks < c (block scan of a chunk histogram) + rank within c.
 template <int NT, int EPT>
-__global__ void __launch_bounds__(NT, 2) topk5_kernel(const uint64_t* __restrict__ cand,
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk5_kernel(const uint64_t* __restrict__ cand,
                                                       const int32_t* __restrict__ cand_count, int cap,
                                                       const int32_t* __restrict__ prefix_len, int n_rows, int k,
                                                       int n_chunks, int32_t* __restrict__ topk, int64_t topk_ld,
@@ -1351,7 +1351,7 @@ static int launch_topk5_t(cudaStream_t st, const uint64_t* cand, const int32_t* 
                           int64_t T, int k, int n_chunks, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
   const size_t bytes = (size_t)kQuadrants * cap * 8 + (size_t)n_chunks * 4 + (((size_t)n_chunks + 7) & ~size_t(7)) * 2 +
                        (size_t)k * (ts ? 8 : 4);
-  if (bytes > 110 * 1024) return -100;
+  if (bytes > 200 * 1024) return -100;
   auto kern = topk5_kernel<NT, EPT>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   int per_sm = 0;
@@ -1372,6 +1372,8 @@ static int launch_topk5(cudaStream_t st, const uint64_t* cand, const int32_t* cc
   if (cap == 256 * 16 / 4) return launch_topk5_t<256, 16>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
   if (cap == 256 * 24 / 4) return launch_topk5_t<256, 24>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
   if (cap == 256 * 32 / 4) return launch_topk5_t<256, 32>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+  if (cap == 512 * 24 / 4) return launch_topk5_t<512, 24>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+  if (cap == 512 * 32 / 4) return launch_topk5_t<512, 32>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
   return -100;
 }
 }  // namespace

@@ -38,6 +38,7 @@ from .config import BLOCK_ATTENTION, ROUTER_KIND_CODE, ROUTER_SCORE_KINDS
 from .validation import check_choice, check_positive_int
 
 METHODS = ("dsa", "misa", "misa_hier")
+V5_CAPS = (512, 1024, 1536, 2048, 3072, 4096)  # per-quadrant capacities of select.cu launch_topk5
 
 
 def _ptr(t):
@@ -244,6 +245,10 @@ class IndexerEngine:
             stride, beta = max(1, self.stride // 2), (self.beta or 1.3)
         stride = max(stride, -(-L // 16384))  # the threshold selector holds <= 16384 samples per row
         cap = int(math.ceil(1.5 * beta * k / 4 / 32)) * 32
+        # round up to a capacity the merge-free selector (select.cu topk5) is compiled for
+        for c in V5_CAPS:
+            if c >= cap:
+                return stride, beta, c
         return stride, beta, cap
 
     def pool(self, x: PreparedInputs):
