@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uin
     pf.n = nx_n;
 #pragma unroll
     for (int q = 0; q < kQuadrants; ++q) pf.c[q] = nx_c[q];
-    if (nx_n <= k && !want_scores) return;  // every prefix token; counts unused (may be unset)
+    if ((nx_n <= k && !want_scores) || nx_n <= 0) return;  // counts unused (may be unset)
     pf.copy = true;
     if (!PF) return;
     uint32_t bytes = 0;
@@ -736,7 +736,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uin
         issue(t + gridDim.x);
         load_meta(t + 2 * gridDim.x);
       }
-      for (int i = threadIdx.x; i < k; i += NT) out[i] = i < n ? i : -1;
+      for (int i = threadIdx.x; i < k; i += NT) {
+        out[i] = i < n ? i : -1;
+        if (outs) outs[i] = -INFINITY;
+      }
       if (threadIdx.x == 0 && flags) flags[t] = 0;
       continue;
     }
@@ -856,7 +859,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk5_kernel(const ui
     pf.n = nx_n;
 #pragma unroll
     for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nx_c[j];
-    if (nx_n <= k && !want_scores) return;
+    // no candidates needed: every prefix token (n <= k) or an empty prefix (counts unset)
+    if ((nx_n <= k && !want_scores) || nx_n <= 0) return;
     uint32_t bytes = 0;
 #pragma unroll
     for (int j = 0; j < kQuadrants; ++j) bytes += ((min(max(nx_c[j], 0), cap) * 8u) + 15u) & ~15u;
@@ -888,13 +892,16 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk5_kernel(const ui
     int32_t* out = topk + (int64_t)t * topk_ld;
     float* outs = want_scores ? topk_scores + (int64_t)t * topk_ld : nullptr;
     const int kk = n < k ? n : k;
-    if (!copy) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73)
+    if (!copy) {  // topk_tokens keeps every prefix token when k >= L (dsa.py:73); empty prefix: none
       __syncthreads();
       if (tid == 0) {
         issue(t + gridDim.x);
         load_meta(t + 2 * gridDim.x);
       }
-      for (int i = tid; i < k; i += NT) out[i] = i < n ? i : -1;
+      for (int i = tid; i < k; i += NT) {
+        out[i] = i < n ? i : -1;
+        if (outs) outs[i] = -INFINITY;
+      }
       if (tid == 0 && flags) flags[t] = 0;
       continue;
     }
