@@ -252,34 +252,115 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int x) {
 }
 
 // ---------------------------------------------------------------- tau ----
+// tau_t = a lower bound of the j-th largest sampled score, j = ceil(beta*k*m/n): the
+// lower edge of the histogram bin that holds it, with 2048 bins over the sampled key
+// range [min, max] (at least 2^-10 relative resolution), so tau never exceeds the j-th
+// value and costs one atomic per sample and three barriers per row.  The kernel is
+// kept lean (registers, 9 KB smem) so that many rows are in flight per SM.
 template <int NT, int EPT>
 __global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__ s, int64_t ld,
                                                        const int32_t* __restrict__ prefix_len, int stride, int k,
                                                        float beta, int64_t append_all, float* __restrict__ tau) {
-  __shared__ SelSh<NT> sh;
-  const int t = blockIdx.x;
+  constexpr int NW = NT / 32, NB = 2048, BPT = NB / NT;
+  __shared__ uint32_t hist[NB];
+  __shared__ uint32_t rmin[NW], rmax[NW];
+  __shared__ int wsum[NW];
+  __shared__ int sh_bin, sh_above, sh_above_new;
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = prefix_len[t];
   if (n <= append_all || n <= k) {
-    if (threadIdx.x == 0) tau[t] = -INFINITY;
+    if (tid == 0) tau[t] = -INFINITY;
     return;
   }
   const int m = (n + stride - 1) / stride;
   long long jj = (long long)ceilf(beta * (float)k * (float)m / (float)n);
   jj = jj < 1 ? 1 : (jj > m ? m : jj);
   const float* row = s + (int64_t)t * ld;
-  uint32_t key[EPT];
+  float x[EPT];
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const int e = r * NT + threadIdx.x;
-    key[r] = e < m ? float_key(row[e]) : 0u;
+    const int e = r * NT + tid;
+    x[r] = row[e < m ? e : 0];
   }
-  int parity = 0, cge, cgt;
-  // tau only has to be a lower bound of the j-th sampled score: resolve the sign, all 8
-  // exponent bits and 7 mantissa bits (key bits 31..16), round the rest down — at most
-  // 2^-7 relative below the exact value (a few more candidates, never fewer)
-  const uint32_t v =
-      kth_largest<NT, EPT>([&](int r) { return key[r]; }, (int)jj, sh, parity, &cge, &cgt, /*min_bit=*/16);
-  if (threadIdx.x == 0) tau[t] = key_float(v);
+  uint32_t key[EPT];
+  uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const bool ok = r * NT + tid < m;
+    key[r] = ok ? float_key(x[r]) : 0u;
+    if (ok) {
+      mn = min(mn, key[r]);
+      mx = max(mx, key[r]);
+    }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) {
+    rmin[w] = mn;
+    rmax[w] = mx;
+  }
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) hist[tid * BPT + i] = 0u;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    mn = min(mn, rmin[i]);
+    mx = max(mx, rmax[i]);
+  }
+  uint32_t lo = mn;
+  uint32_t span = mx - mn;  // window [lo, lo + span]
+  int sft = span == 0u ? 0 : max(0, 32 - __clz(span) - 11);
+  // level 1 bins the whole sampled range; a coarse boundary bin (wider than 2^12 key ulps,
+  // i.e. ~2^-11 relative) is re-binned once at 2^-11 of its width
+  for (int level = 0;; ++level) {
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const uint32_t d = key[r] - lo;
+      if (key[r] && key[r] >= lo && d <= span) atomicAdd(&hist[d >> sft], 1u);
+    }
+    __syncthreads();
+    // thread tid owns bins [NB - BPT*(tid+1), NB - BPT*tid): descending keys
+    uint32_t c[BPT];
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+      c[i] = hist[NB - 1 - (tid * BPT + i)];
+      tot += (int)c[i];
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int above = incl - tot + (level ? sh_above : 0);
+    for (int i = 0; i < w; ++i) above += wsum[i];
+    if (above < jj && jj <= above + tot) {
+#pragma unroll
+      for (int i = 0; i < BPT; ++i) {
+        if (above < jj && jj <= above + (int)c[i]) {
+          sh_bin = NB - 1 - (tid * BPT + i);
+          sh_above_new = above;
+        }
+        above += (int)c[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) hist[tid * BPT + i] = 0u;
+    __syncthreads();
+    const uint32_t b = (uint32_t)sh_bin;
+    lo += b << sft;
+    if (level == 1 || sft <= 12) {
+      if (tid == 0) tau[t] = key_float(lo);  // lower edge of the bin: <= the j-th sample
+      return;
+    }
+    span = (1u << sft) - 1u;
+    sft = sft - 11;
+    if (tid == 0) sh_above = sh_above_new;  // samples above the refined window
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------- v3 row selector core ----
