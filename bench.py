@@ -44,7 +44,7 @@ METRIC = "indexer ms/layer at 128K (H^I=64,h=8) + speedup vs dense DSA; top-k re
 def _args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--L", type=int, default=131072)
@@ -88,7 +88,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -138,7 +138,7 @@ def run_reference(a):
     gen = torch.Generator().manual_seed(0)
     K = torch.randn(a.L, a.d, generator=gen).bfloat16().double().numpy()
     cores = os.cpu_count() or 1
-    rows = cpu_bench.sample_rows(a.L, a.L, max(16, 2 * cores))
+    rows = cpu_bench.sample_rows(a.L, a.L, max(64, 8 * cores))
     rng = np.random.default_rng(0)
     Qr = O.bf16_round(rng.standard_normal((len(rows), a.H, a.d)))
     Wr = O.softmax_rows(rng.standard_normal((len(rows), a.H)))
@@ -356,7 +356,7 @@ def run_ours(a):
     if not a.no_cpu and world == 1:
         from oracle import cpu_bench
         cores = os.cpu_count() or 1
-        srows = cpu_bench.sample_rows(L, T, max(16, 2 * cores))
+        srows = cpu_bench.sample_rows(L, T, max(64, 8 * cores))
         Qs = Q[torch.as_tensor(srows)].double().cpu().numpy()
         Ws = W[torch.as_tensor(srows)].double().cpu().numpy()
         info = cpu_bench.time_layer("misa", Kn, Qs, Ws, srows, L, T, k=a.k, h=a.h, B=a.B, kp=a.kprime, cores=cores)
