@@ -131,6 +131,7 @@ struct ScoreArgs {
   const int32_t* __restrict__ prefix_len;
   const int32_t* __restrict__ items;
   const int32_t* __restrict__ item_tiles;
+  const int32_t* __restrict__ item_tile0;  // MATERIALIZE key split: first tile of item i (null: 0)
   int n_items;
   int T, H, Hp;
   int key_stride;
@@ -229,12 +230,14 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         const int idx = item_index(it, P, bid);
         if (idx >= a.n_items) break;
         const int nt = a.item_tiles[idx];
+        const int j0 = a.item_tile0 ? a.item_tile0[idx] : 0;
         for (int j = 0; j < nt; ++j) {
           ptx::mbar_wait(&empty_a[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
 #pragma unroll
           for (int at = 0; at < D / 64; ++at)
-            ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_k, &full_a[s], at * 64, j * kTileKeys);
+            ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_k, &full_a[s], at * 64,
+                             (j0 + j) * kTileKeys);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -286,6 +289,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
       const int idx = item_index(it, P, bid);
       if (idx >= a.n_items) break;
       const int nt = a.item_tiles[idx];
+      const int j0 = a.item_tile0 ? a.item_tile0[idx] : 0;
       const int row0 = a.items[idx] * G;
 
       // B operand: row r = q*HQ + j <- Q[row0+q][head(q,j)][:], SW128 K-major layout.
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
           sc[1] = gate_relu_pair8(v0, 2, wp);
           sc[2] = gate_relu_pair8(v1, 0, wp);
           sc[3] = gate_relu_pair8(v1, 2, wp);
-          const int kq = jt * kTileKeys + quad * 32;
+          const int kq = (j0 + jt) * kTileKeys + quad * 32;
           if constexpr (FILTER) {
             uint32_t bal[4][2];
             if (kq + 31 >= lim_min)  // warp-uniform: only the diagonal tile tests the prefix bound
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         for (int jt = 0; jt < nt; ++jt) {
           ptx::mbar_wait(&tfull[acc], aph);
           ptx::tc_fence_after();
-          const int key0 = jt * kTileKeys + quad * 32;
+          const int key0 = (j0 + jt) * kTileKeys + quad * 32;
           const int key = key0 + lane;
           const uint32_t taddr =
               tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kTileCols + split * C::COLS;
@@ -544,11 +548,12 @@ static int check_common(int64_t n_keys, int D, int n_heads, int n_heads_pad, int
 
 using namespace misa;
 
-extern "C" int misa_score_materialize(const void* keys, int64_t n_keys, int64_t key_stride, int head_dim,
-                                      const void* queries, const float* weights, int n_heads, int n_heads_pad,
-                                      const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
-                                      int64_t n_rows, const int32_t* items, const int32_t* item_tiles, int n_items,
-                                      float* out, int64_t out_ld, void* stream) {
+extern "C" int misa_score_materialize_split(const void* keys, int64_t n_keys, int64_t key_stride, int head_dim,
+                                            const void* queries, const float* weights, int n_heads, int n_heads_pad,
+                                            const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
+                                            int64_t n_rows, const int32_t* items, const int32_t* item_tiles,
+                                            const int32_t* item_tile0, int n_items, float* out, int64_t out_ld,
+                                            void* stream) {
   int rc = check_common(n_keys, head_dim, n_heads, n_heads_pad, heads_per_query, n_rows, keys, queries, weights,
                         prefix_len, items, item_tiles, n_items);
   if (rc) return rc;
@@ -566,6 +571,7 @@ extern "C" int misa_score_materialize(const void* keys, int64_t n_keys, int64_t 
   a.prefix_len = prefix_len;
   a.items = items;
   a.item_tiles = item_tiles;
+  a.item_tile0 = item_tile0;
   a.n_items = n_items;
   a.T = static_cast<int>(n_rows);
   a.H = n_heads;
@@ -574,6 +580,16 @@ extern "C" int misa_score_materialize(const void* keys, int64_t n_keys, int64_t 
   a.out = out;
   a.out_ld = out_ld;
   return dispatch_score<false>(head_dim, heads_per_query, map, a, as_stream(stream));
+}
+
+extern "C" int misa_score_materialize(const void* keys, int64_t n_keys, int64_t key_stride, int head_dim,
+                                      const void* queries, const float* weights, int n_heads, int n_heads_pad,
+                                      const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
+                                      int64_t n_rows, const int32_t* items, const int32_t* item_tiles, int n_items,
+                                      float* out, int64_t out_ld, void* stream) {
+  return misa_score_materialize_split(keys, n_keys, key_stride, head_dim, queries, weights, n_heads, n_heads_pad,
+                                      heads, heads_per_query, prefix_len, n_rows, items, item_tiles, nullptr, n_items,
+                                      out, out_ld, stream);
 }
 
 extern "C" int misa_score_filter(const void* keys, int64_t n_keys, int head_dim, const void* queries,

@@ -964,6 +964,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk5_kernel(const ui
   for (int t = blockIdx.x; t < n_rows; t += gridDim.x) {
     __syncthreads();
     const int ti_ = (t - blockIdx.x) / gridDim.x;
+    (void)ti_;
     SEL_MARK(ti_, 0);
     const int n = pf.n;
     const bool copy = pf.copy;
@@ -1241,9 +1242,7 @@ __global__ void __launch_bounds__(kGlbThreads) dense_global_kernel(const float* 
                                                                    const int32_t* __restrict__ rows, int k,
                                                                    int32_t* __restrict__ topk, int64_t topk_ld,
                                                                    float* __restrict__ topk_scores) {
-  extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ GlbShared sh;
-  __shared__ int counter;
   const int r = rows ? rows[blockIdx.x] : blockIdx.x;
   const int n = row_len[r];
   const float* row = s + (int64_t)r * ld;
@@ -1264,27 +1263,52 @@ __global__ void __launch_bounds__(kGlbThreads) dense_global_kernel(const float* 
       thr = (int)~glb_radix_select(tie_key, n, j_rem, sh, &jr2, &ce2);
     }
   }
-  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
-  float* csc = reinterpret_cast<float*>(dsm + (size_t)k * 4);
-  if (threadIdx.x == 0) counter = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += kGlbThreads) {
-    const uint32_t kv = key_of(i);
-    if (kk > 0 && (kk >= n || kv > v || (kv == v && idx_of(i) <= thr))) {
-      const int p = atomicAdd(&counter, 1);
-      if (p < kk) {
-        cidx[p] = idx_of(i);
-        csc[p] = key_float(kv);
+  // ordered compaction: 16 consecutive candidates per thread per round (thread-major), one
+  // block scan per round, so the output is ascending without a sort
+  constexpr int kPer = 16, kRound = kGlbThreads * kPer;
+  constexpr int NW = kGlbThreads / 32;
+  __shared__ int wtot[NW];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int base = 0;
+  for (int r0 = 0; r0 < n && base < kk; r0 += kRound) {
+    const int i0 = r0 + threadIdx.x * kPer;
+    uint32_t selm = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int i = i0 + e;
+      if (i < n) {
+        const uint32_t kv = key_of(i);
+        const bool sel = kk >= n || kv > v || (kv == v && idx_of(i) <= thr);
+        selm |= (sel ? 1u : 0u) << e;
       }
     }
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < kk; p += kGlbThreads) {
-    const int x = cidx[p];
-    int pos = 0;
-    for (int q = 0; q < kk; ++q) pos += cidx[q] < x;
-    out[pos] = x;
-    if (outs) outs[pos] = csc[p];
+    const int c = __popc(selm);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wtot[w] = incl;
+    __syncthreads();
+    int pos = base + incl - c;
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      pos += i < w ? wtot[i] : 0;
+      tot += wtot[i];
+    }
+    while (selm) {
+      const int e = __ffs(selm) - 1;
+      selm &= selm - 1;
+      if (pos < kk) {
+        out[pos] = idx_of(i0 + e);
+        if (outs) outs[pos] = row[i0 + e];
+      }
+      ++pos;
+    }
+    base += tot;
+    __syncthreads();
   }
   for (int i = kk + threadIdx.x; i < k; i += kGlbThreads) {
     out[i] = -1;
@@ -1504,9 +1528,7 @@ extern "C" int misa_select_dense(const float* scores, int64_t ld, const int32_t*
   int rc = dispatch_capacity<DenseL>(ld, st, scores, ld, idx, idx_ld, row_len, rows, n_rows, k, topk, topk_ld,
                                      topk_scores);
   if (rc != -100) return rc;
-  const size_t gb = (size_t)k * 8;
-  MISA_CUDA_TRY(cudaFuncSetAttribute(dense_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb));
-  dense_global_kernel<<<(unsigned)n_rows, kGlbThreads, gb, st>>>(scores, ld, idx, idx_ld, row_len, rows, k, topk,
+  dense_global_kernel<<<(unsigned)n_rows, kGlbThreads, 0, st>>>(scores, ld, idx, idx_ld, row_len, rows, k, topk,
                                                                  topk_ld, topk_scores);
   MISA_LAUNCH_CHECK();
   return MISA_OK;

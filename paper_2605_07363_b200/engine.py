@@ -262,8 +262,11 @@ class IndexerEngine:
         _lib.call("misa_pool_keys", _ptr(x.keys), x.L, x.D, self.B, _ptr(P), None, _ptr(planes), rows, self._stream())
         return P, planes, n_chunks, rows
 
-    def route(self, x: PreparedInputs, need_importance: bool = False):
-        """K2: heads (T, hq) int32 ascending, -1 padded; importance (T, Hp) f32 or None."""
+    def route(self, x: PreparedInputs, need_importance: bool = False, cache=None):
+        """K2: heads (T, hq) int32 ascending, -1 padded; importance (T, Hp) f32 or None.
+
+        With a ``PooledKeyCache`` the router reads its incrementally maintained prefix sums
+        and pooled planes (``pooling.py:87-115``) instead of re-pooling the prefix."""
         h = min(self.h, x.H)
         hq = heads_per_query(h)
         dev = x.keys.device
@@ -272,7 +275,13 @@ class IndexerEngine:
         imp = self._buf("importance", (x.T, x.Hp), torch.float32, dev) if need_importance else None
         partial, n_chunks = None, 1
         if self.router_score == BLOCK_ATTENTION:
-            P, planes, n_chunks, rows = self.pool(x)
+            if cache is not None:
+                if cache.B != self.B:
+                    raise ValueError(f"cache block size {cache.B} != engine block_size {self.B}")
+                P, planes, rows = cache.prefix, cache.planes, cache.rows
+                n_chunks = max(1, (x.L // self.B + 127) // 128)
+            else:
+                P, planes, n_chunks, rows = self.pool(x)
             key = ("route", x.causal_key or x.prefix_host.tobytes(), x.Hp, self.B, n_chunks)
             it_tile, it_chunk, it_cols = self._dev_list(key, lambda: self._route_items(x.prefix_host, x.Hp, n_chunks),
                                                         dev)
@@ -373,6 +382,86 @@ class IndexerEngine:
         _lib.call("misa_select_dense", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), None, x.T, k,
                   _ptr(out), out.stride(0), None, stream)
         self._mark("refine:end")
+
+    # ----------------------------------------------------------- decode
+    @staticmethod
+    def split_items(lens: np.ndarray, G: int, target_items: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """Groups of G rows, each group's 128-key tiles split into chunks so that about
+        ``target_items`` work items exist (key-axis split for few rows x long prefixes)."""
+        T = lens.shape[0]
+        ng = (T + G - 1) // G
+        pad = np.zeros(ng * G, dtype=np.int64)
+        pad[:T] = lens
+        tiles = (pad.reshape(ng, G).max(1) + 127) // 128
+        total = int(tiles.sum())
+        chunk = max(4, -(-total // max(1, target_items)))
+        it_g, it_n, it_0 = [], [], []
+        for g in range(ng):
+            for t0 in range(0, int(tiles[g]), chunk):
+                it_g.append(g)
+                it_0.append(t0)
+                it_n.append(min(chunk, int(tiles[g]) - t0))
+        order = np.argsort(-np.asarray(it_n), kind="stable")
+        return (np.asarray(it_g, np.int32)[order], np.asarray(it_n, np.int32)[order],
+                np.asarray(it_0, np.int32)[order])
+
+    def dense_scores(self, x: PreparedInputs, heads, hq: int) -> torch.Tensor:
+        """(T, L) f32 score rows (valid up to each prefix), key-axis split across the SMs."""
+        dev = x.keys.device
+        G = 256 // hq
+        ckey = x.causal_key or x.prefix_host.tobytes()
+        target = 4 * _lib.load().misa_sm_count()
+        items, tiles, tile0 = self._dev_list(("split", ckey, G, target),
+                                             lambda: self.split_items(x.prefix_host, G, target), dev)
+        rows = self._buf("dense_rows", (x.T, x.L), torch.float32, dev)
+        self._mark("decode:score")
+        _lib.call("misa_score_materialize_split", _ptr(x.keys), x.L, 1, x.D, _ptr(x.queries), _ptr(x.weights), x.H,
+                  x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles), _ptr(tile0), items.numel(),
+                  _ptr(rows), x.L, self._stream())
+        return rows
+
+    def decode(self, keys=None, queries=None, weights=None, prefix_len=None, *, cache=None,
+               need_importance: bool = False, out: torch.Tensor | None = None) -> IndexerOutput:
+        """Decode step: a few query rows (T <= a few hundred) against long prefixes.
+
+        Scores are materialised with the key axis split across the SMs (a causal-prefill
+        work item is a whole row group, which would leave most SMs idle here) and each row
+        takes the exact long-row selector; with ``cache`` (a ``PooledKeyCache``) the keys
+        and the router's pooled state come from the incrementally maintained cache.
+        Row t equals the reference on ``IndexerWorkload(K[:n_t], Q[t], W[t])``; the
+        default prefix is the whole cache / key set for every row."""
+        if cache is not None:
+            keys = cache.keys[:cache.length, :cache.d]
+        if keys is None or queries is None or weights is None:
+            raise ValueError("decode needs keys (or a cache), queries and weights")
+        Tq = int(queries.shape[0])
+        L = int(keys.shape[0])
+        if prefix_len is None:
+            prefix_len = np.full(Tq, L, dtype=np.int64)
+        x = prepare_inputs(keys, queries, weights, prefix_len)
+        dev = x.keys.device
+        k = self.k
+        if out is None:
+            out = torch.empty(x.T, k, dtype=torch.int32, device=dev)
+        heads, hq, imp = None, x.Hp, None
+        if self.method != "dsa":
+            heads, hq, imp = self.route(x, need_importance, cache=cache)
+        kk = k if self.method != "misa_hier" else max(self.kprime, k)
+        rows = self.dense_scores(x, heads, hq)
+        tgt = out if self.method != "misa_hier" else self._buf("hier_cand", (x.T, kk), torch.int32, dev)
+        self._mark("decode:select")
+        _lib.call("misa_select_dense", _ptr(rows), x.L, None, 0, _ptr(x.prefix), None, x.T, kk, _ptr(tgt),
+                  tgt.stride(0), None, self._stream())
+        self._mark("decode:end")
+        self.last_fallback_rows = 0
+        h = min(self.h, x.H)
+        if self.method == "dsa":
+            return IndexerOutput(topk=out)
+        if self.method == "misa":
+            return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H])
+        self.refine(x, tgt, k, out)
+        return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H],
+                             candidates=tgt)
 
     # ----------------------------------------------------------- entry
     def run(self, keys, queries, weights, prefix_len=None, *, need_importance: bool = False,
