@@ -27,6 +27,7 @@
  *   misa_select_threshold (no reference counterpart: sampled threshold for the fused top-k)
  *   misa_select_topk      dsa.py:64-76       topk_tokens over the filtered candidates
  *   misa_select_dense     dsa.py:64-92       topk_tokens / topk_within over a dense score row
+ *   misa_select_dense_long dsa.py:64-76      topk_tokens over long dense rows (decode), all SMs
  *   misa_refine_scores    dsa.py:95-115      dsa_rescore (MISA-dagger fine stage), routing.py:144-174
  *   misa_merge_topk       (no reference counterpart: key-sharded multi-GPU merge)
  *   misa_shard_map_indices (no reference counterpart: local -> global key index of a shard)
@@ -137,6 +138,17 @@ int misa_select_topk(const uint64_t* cand, const int32_t* cand_count, int cap, c
 int misa_select_dense(const float* scores, int64_t ld, const int32_t* idx, int64_t idx_ld, const int32_t* row_len,
                       const int32_t* rows, int64_t n_rows, int k, int32_t* topk, int64_t topk_ld,
                       float* topk_scores, void* stream);
+
+/* Exact top-k over long dense rows (decode: few rows x up to millions of keys) using all
+ * SMs: tau[t] from a 1/32-strided sample (j = beta*k/32), per-4096-key segment counts
+ * (seg_cnt: n_rows x ceil(max_len/4096)), index-ordered compaction of scores >= tau into
+ * cand_scores / cand_idx (n_rows x cap, cand_count[t] = total), the register selector on the
+ * candidates, and an on-device exact re-selection of rows whose count fell outside
+ * [min(k, n), cap].  Same output contract as misa_select_dense. */
+int misa_select_dense_long(const float* scores, int64_t ld, const int32_t* row_len, int64_t n_rows, int k,
+                           int64_t max_len, float beta, float* tau, int32_t* seg_cnt, float* cand_scores,
+                           int32_t* cand_idx, int32_t* cand_count, int cap, int32_t* topk, int64_t topk_ld,
+                           float* topk_scores, void* stream);
 
 /* MISA-dagger fine stage: out[t*out_ld + i] = sum_j w_tj ReLU(q_tj . key[cand[t][i]]) over all
  * heads, for i < n_cand[t] (cand ascending, -1 padded), for the rows listed in rows[0..n_items)

@@ -41,6 +41,8 @@ SIGNATURES: dict[str, list] = {
     "misa_select_threshold": [_vp, _i64, _vp, _i64, _i32, _i32, _f32, _i64, _vp, _vp],
     "misa_select_topk": [_vp, _vp, _i32, _vp, _i64, _i32, _i64, _vp, _i64, _vp, _vp, _vp],
     "misa_select_dense": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _vp, _vp],
+    "misa_select_dense_long": [_vp, _i64, _vp, _i64, _i32, _i64, _f32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i64,
+                               _vp, _vp],
     "misa_refine_scores": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
                            _vp],
     "misa_merge_topk": [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _vp, _i64, _vp],

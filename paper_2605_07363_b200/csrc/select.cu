@@ -260,7 +260,8 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int x) {
 template <int NT, int EPT>
 __global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__ s, int64_t ld,
                                                        const int32_t* __restrict__ prefix_len, int stride, int k,
-                                                       float beta, int64_t append_all, float* __restrict__ tau) {
+                                                       float beta, int64_t append_all, float* __restrict__ tau,
+                                                       int elem_step = 1) {
   constexpr int NW = NT / 32, NB = 2048, BPT = NB / NT;
   __shared__ uint32_t hist[NB];
   __shared__ uint32_t rmin[NW], rmax[NW];
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int e = r * NT + tid;
-    x[r] = row[e < m ? e : 0];
+    x[r] = row[(int64_t)(e < m ? e : 0) * elem_step];
   }
   uint32_t key[EPT];
   uint32_t mn = 0xffffffffu, mx = 0u;
@@ -1132,7 +1133,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ SelSh<NT> sh;
   const int rr = rows ? rows[blockIdx.x] : blockIdx.x;
-  const int n = row_len[rr];
+  const int n = min(row_len[rr], (int)ld);  // candidate counts may exceed the staged capacity
   const float* row = s + (int64_t)rr * ld;
   const int32_t* irow = idx ? idx + (int64_t)rr * idx_ld : nullptr;
   int32_t* out = topk + (int64_t)rr * topk_ld;
@@ -1176,74 +1177,145 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
 // Global path for rows longer than the register capacity (exact fallback): MSB radix
 // passes over global memory with smem histograms, then rank-by-comparison ordering.
 constexpr int kGlbThreads = 256;
+constexpr int kGlbBins = 2048;
 struct GlbShared {
-  uint32_t hist[256];
-  uint32_t red[kGlbThreads / 32];
+  uint32_t hist[kGlbBins];
+  uint32_t red[kGlbThreads / 32], red2[kGlbThreads / 32];
   int info[4];
 };
 
 template <typename KeyFn>
 __device__ uint32_t glb_radix_select(KeyFn key_of, int N, int j, GlbShared& sh, int* j_rem_out, int* cnt_eq_out) {
-  const uint32_t first = key_of(0);
-  uint32_t diff = 0;
-  for (int i = threadIdx.x; i < N; i += kGlbThreads) diff |= key_of(i) ^ first;
-  diff = __reduce_or_sync(0xffffffffu, diff);
-  if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = diff;
-  __syncthreads();
-  diff = 0;
-  for (int i = 0; i < kGlbThreads / 32; ++i) diff |= sh.red[i];
-  __syncthreads();
-  if (diff == 0) {
-    *j_rem_out = j;
-    *cnt_eq_out = N;
-    return first;
+  // j-th largest key of a long row streamed from global by one CTA: a min/max pass, then
+  // affine windows of 2048 bins over [lo, hi] (scores spread over many bins, so the smem
+  // atomics rarely collide), each level narrowing to the boundary bin until it is a
+  // single key value.  Returns the value; *j_rem_out = rank of the cut among the keys
+  // equal to it, *cnt_eq_out = how many keys equal it.
+  constexpr int NW = kGlbThreads / 32, NB = kGlbBins, BPT = NB / kGlbThreads;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  for (int i0 = threadIdx.x; i0 < N; i0 += kGlbThreads * 8) {
+    uint32_t kv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * kGlbThreads;
+      kv[u] = i < N ? key_of(i) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u * kGlbThreads < N) {
+        mn = min(mn, kv[u]);
+        mx = max(mx, kv[u]);
+      }
   }
-  int hi = 31 - __clz(diff);
-  uint32_t prefix = (hi == 31) ? 0u : (first & ~((2u << hi) - 1u));
-  int j_rem = j, cnt_eq = 0;
-  while (hi >= 0) {
-    const int lo = hi >= 7 ? hi - 7 : 0;
-    const uint32_t dmask = (1u << (hi - lo + 1)) - 1u;
-    const uint32_t mhi = (hi == 31) ? 0u : ~((2u << hi) - 1u);
-    for (int i = threadIdx.x; i < 256; i += kGlbThreads) sh.hist[i] = 0;
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) {
+    sh.red[w] = mn;
+    sh.red2[w] = mx;
+  }
+  __syncthreads();
+  mn = sh.red[0];
+  mx = sh.red2[0];
+  for (int i = 1; i < NW; ++i) {
+    mn = min(mn, sh.red[i]);
+    mx = max(mx, sh.red2[i]);
+  }
+  uint32_t lo = mn, span = mx - mn;  // window [lo, lo + span]
+  const int need = j;  // absolute rank: keys above the window are counted in every level
+  for (;;) {
+    if (span == 0u) {  // one key value left: count the keys equal to / above it
+      int ceq = 0, cgt = 0;
+      for (int i = threadIdx.x; i < N; i += kGlbThreads) {
+        const uint32_t kv = key_of(i);
+        ceq += kv == lo;
+        cgt += kv > lo;
+      }
+      ceq = __reduce_add_sync(0xffffffffu, ceq);
+      cgt = __reduce_add_sync(0xffffffffu, cgt);
+      __syncthreads();
+      if (lane == 0) {
+        sh.red[w] = (uint32_t)ceq;
+        sh.red2[w] = (uint32_t)cgt;
+      }
+      __syncthreads();
+      int teq = 0, tgt = 0;
+      for (int i = 0; i < NW; ++i) {
+        teq += (int)sh.red[i];
+        tgt += (int)sh.red2[i];
+      }
+      __syncthreads();
+      *j_rem_out = j - tgt;
+      *cnt_eq_out = teq;
+      return lo;
+    }
+    const int sft = max(0, 32 - __clz(span) - 11);
+    for (int i = threadIdx.x; i < NB; i += kGlbThreads) sh.hist[i] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < N; i += kGlbThreads) {
-      const uint32_t k = key_of(i);
-      if ((k & mhi) == (prefix & mhi)) atomicAdd(&sh.hist[(k >> lo) & dmask], 1u);
+    int above = 0;
+    for (int i0 = threadIdx.x; i0 < N; i0 += kGlbThreads * 8) {
+      uint32_t kv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kGlbThreads;
+        kv[u] = i < N ? key_of(i) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (i0 + u * kGlbThreads < N && kv[u] >= lo) {
+          const uint32_t d = kv[u] - lo;
+          if (d <= span) atomicAdd(&sh.hist[d >> sft], 1u);
+          else ++above;
+        }
+      }
+    }
+    above = __reduce_add_sync(0xffffffffu, above);
+    if (lane == 0) sh.red[w] = (uint32_t)above;
+    __syncthreads();
+    int ab = 0;
+    for (int i = 0; i < NW; ++i) ab += (int)sh.red[i];
+    // thread owns bins [NB - BPT*(tid+1), NB - BPT*tid) (descending)
+    uint32_t c[BPT];
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+      c[i] = sh.hist[NB - 1 - (threadIdx.x * BPT + i)];
+      tot += (int)c[i];
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t above = 0;
-      for (int d = (int)dmask; d >= 0; --d) {
-        if ((uint32_t)j_rem <= above + sh.hist[d]) {
-          sh.info[0] = d;
-          sh.info[1] = (int)above;
-          sh.info[2] = (int)sh.hist[d];
-          break;
+    if (lane == 31) sh.red2[w] = (uint32_t)incl;
+    __syncthreads();
+    int ex = ab + incl - tot;
+    for (int i = 0; i < w; ++i) ex += (int)sh.red2[i];
+    if (ex < need && need <= ex + tot) {
+#pragma unroll
+      for (int i = 0; i < BPT; ++i) {
+        if (ex < need && need <= ex + (int)c[i]) {
+          sh.info[0] = NB - 1 - (threadIdx.x * BPT + i);
+          sh.info[1] = ex;
         }
-        above += sh.hist[d];
+        ex += (int)c[i];
       }
     }
     __syncthreads();
-    j_rem -= sh.info[1];
-    cnt_eq = sh.info[2];
-    prefix |= (uint32_t)sh.info[0] << lo;
+    const uint32_t b = (uint32_t)sh.info[0];
+    // the next window is bin b: [lo + (b << sft), lo + ((b + 1) << sft) - 1] within [lo, lo + span]
+    lo += b << sft;
+    span = min(span - (b << sft), sft >= 32 ? 0xffffffffu : ((1u << sft) - 1u));
     __syncthreads();
-    hi = lo - 1;
   }
-  *j_rem_out = j_rem;
-  *cnt_eq_out = cnt_eq;
-  return prefix;
 }
 
-__global__ void __launch_bounds__(kGlbThreads) dense_global_kernel(const float* __restrict__ s, int64_t ld,
-                                                                   const int32_t* __restrict__ idx, int64_t idx_ld,
-                                                                   const int32_t* __restrict__ row_len,
-                                                                   const int32_t* __restrict__ rows, int k,
-                                                                   int32_t* __restrict__ topk, int64_t topk_ld,
-                                                                   float* __restrict__ topk_scores) {
+__device__ void dense_global_row(const float* __restrict__ s, int64_t ld, const int32_t* __restrict__ idx,
+                                 int64_t idx_ld, const int32_t* __restrict__ row_len, int r, int k,
+                                 int32_t* __restrict__ topk, int64_t topk_ld, float* __restrict__ topk_scores) {
   __shared__ GlbShared sh;
-  const int r = rows ? rows[blockIdx.x] : blockIdx.x;
   const int n = row_len[r];
   const float* row = s + (int64_t)r * ld;
   const int32_t* irow = idx ? idx + (int64_t)r * idx_ld : nullptr;
@@ -1314,6 +1386,121 @@ __global__ void __launch_bounds__(kGlbThreads) dense_global_kernel(const float* 
     out[i] = -1;
     if (outs) outs[i] = -INFINITY;
   }
+}
+
+__global__ void __launch_bounds__(kGlbThreads) dense_global_kernel(const float* __restrict__ s, int64_t ld,
+                                                                   const int32_t* __restrict__ idx, int64_t idx_ld,
+                                                                   const int32_t* __restrict__ row_len,
+                                                                   const int32_t* __restrict__ rows, int k,
+                                                                   int32_t* __restrict__ topk, int64_t topk_ld,
+                                                                   float* __restrict__ topk_scores) {
+  dense_global_row(s, ld, idx, idx_ld, row_len, rows ? rows[blockIdx.x] : blockIdx.x, k, topk, topk_ld, topk_scores);
+}
+
+// ------------------------------------------- long dense rows, many CTAs ----
+// Decode rows (few rows x up to 1M keys): a 1/32-strided sample gives tau_t (as in the
+// fused prefill selector), every CTA then counts and compacts its 4096-key segment's
+// scores >= tau_t in index order into the row's candidate list (two passes, all SMs),
+// and the register selector finishes on <= cap candidates.  Rows whose candidates
+// under/overflow are flagged for the single-CTA exact path.
+constexpr int kSegThreads = 256, kSegPer = 16, kSeg = kSegThreads * kSegPer;
+
+__global__ void __launch_bounds__(kSegThreads) seg_count_kernel(const float* __restrict__ s, int64_t ld,
+                                                               const int32_t* __restrict__ row_len,
+                                                               const float* __restrict__ tau,
+                                                               int32_t* __restrict__ seg_cnt, int n_seg) {
+  const int t = blockIdx.y, sg = blockIdx.x;
+  const int n = row_len[t];
+  const float tv = tau[t];
+  const float* row = s + (int64_t)t * ld;
+  const int i0 = sg * kSeg + threadIdx.x * kSegPer;
+  float x[kSegPer];
+#pragma unroll
+  for (int e = 0; e < kSegPer; ++e) x[e] = i0 + e < n ? row[i0 + e] : -INFINITY;
+  int c = 0;
+#pragma unroll
+  for (int e = 0; e < kSegPer; ++e) c += (i0 + e < n) && x[e] >= tv;
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ int ws[kSegThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < kSegThreads / 32; ++i) tot += ws[i];
+    seg_cnt[(int64_t)t * n_seg + sg] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_compact_kernel(const float* __restrict__ s, int64_t ld,
+                                                                 const int32_t* __restrict__ row_len,
+                                                                 const float* __restrict__ tau,
+                                                                 const int32_t* __restrict__ seg_cnt, int n_seg,
+                                                                 float* __restrict__ cs, int32_t* __restrict__ ci,
+                                                                 int cap, int32_t* __restrict__ cnt_out) {
+  constexpr int NW = kSegThreads / 32;
+  __shared__ int ws[NW];
+  __shared__ int sbase;
+  const int t = blockIdx.y, sg = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n = row_len[t];
+  const float tv = tau[t];
+  const float* row = s + (int64_t)t * ld;
+  // base = candidates of the row's earlier segments
+  int b = 0;
+  for (int i = threadIdx.x; i < sg; i += kSegThreads) b += seg_cnt[(int64_t)t * n_seg + i];
+  b = __reduce_add_sync(0xffffffffu, b);
+  if (lane == 0) ws[w] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < NW; ++i) tot += ws[i];
+    sbase = tot;
+  }
+  __syncthreads();
+  const int base = sbase;
+  const int i0 = sg * kSeg + threadIdx.x * kSegPer;
+  float x[kSegPer];
+#pragma unroll
+  for (int e = 0; e < kSegPer; ++e) x[e] = i0 + e < n ? row[i0 + e] : -INFINITY;
+  uint32_t selm = 0;
+#pragma unroll
+  for (int e = 0; e < kSegPer; ++e) selm |= ((i0 + e < n) && x[e] >= tv ? 1u : 0u) << e;
+  const int c = __popc(selm);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) ws[w] = incl;
+  __syncthreads();
+  int pos = base + incl - c;
+  for (int i = 0; i < w; ++i) pos += ws[i];
+#pragma unroll
+  for (int e = 0; e < kSegPer; ++e) {
+    if ((selm >> e) & 1u) {
+      if (pos < cap) {
+        cs[(int64_t)t * cap + pos] = x[e];
+        ci[(int64_t)t * cap + pos] = i0 + e;
+      }
+      ++pos;
+    }
+  }
+  if (sg == n_seg - 1 && threadIdx.x == kSegThreads - 1) cnt_out[t] = pos;  // row total (may exceed cap)
+}
+
+// Rows whose candidate count is outside [min(k, n), cap] are re-selected exactly by the
+// single-CTA path (the others exit at once), so no host round trip is needed.
+__global__ void __launch_bounds__(kGlbThreads) seg_fixup_kernel(const float* __restrict__ s, int64_t ld,
+                                                               const int32_t* __restrict__ row_len,
+                                                               const int32_t* __restrict__ cnt, int cap, int k,
+                                                               int32_t* __restrict__ topk, int64_t topk_ld,
+                                                               float* __restrict__ topk_scores) {
+  const int t = blockIdx.x;
+  const int n = row_len[t];
+  const int c = cnt[t];
+  if (c >= (n < k ? n : k) && c <= cap) return;
+  dense_global_row(s, ld, nullptr, 0, row_len, t, k, topk, topk_ld, topk_scores);
 }
 
 // -------------------------------------------------- multi-GPU merge ----
@@ -1403,6 +1590,16 @@ struct ThresholdL {
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
                 float beta, int64_t aa, float* tau) {
     threshold_kernel<NT, EPT><<<(unsigned)T, NT, 0, st>>>(s, ld, pl, stride, k, beta, aa, tau);
+    MISA_LAUNCH_CHECK();
+    return MISA_OK;
+  }
+};
+
+template <int NT, int EPT>
+struct ThresholdStepL {  // samples every `stride`-th element of a dense row
+  static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
+                float beta, int64_t aa, float* tau) {
+    threshold_kernel<NT, EPT><<<(unsigned)T, NT, 0, st>>>(s, ld, pl, stride, k, beta, aa, tau, stride);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
   }
@@ -1543,4 +1740,44 @@ extern "C" int misa_merge_topk(const float* part_scores, const int32_t* part_idx
                                            n_parts, part_stride, n_rows, k_in, k, topk, topk_ld);
   MISA_REQUIRE(rc != -100, "n_parts*k_in exceeds the register selector");
   return rc;
+}
+
+static int misa_select_dense_clamped(const float* cs, int64_t ld, const int32_t* ci, int64_t ci_ld,
+                                     const int32_t* cnt, int64_t n_rows, int k, int32_t* topk, int64_t topk_ld,
+                                     float* topk_scores, cudaStream_t st) {
+  const int rc = dispatch_capacity<DenseL>(ld, st, cs, ld, ci, ci_ld, cnt, nullptr, n_rows, k, topk, topk_ld,
+                                           topk_scores);
+  MISA_REQUIRE(rc != -100, "candidate capacity %lld exceeds the register selector", (long long)ld);
+  return rc;
+}
+
+extern "C" int misa_select_dense_long(const float* scores, int64_t ld, const int32_t* row_len, int64_t n_rows,
+                                      int k, int64_t max_len, float beta, float* tau, int32_t* seg_cnt,
+                                      float* cand_scores, int32_t* cand_idx, int32_t* cand_count, int cap,
+                                      int32_t* topk, int64_t topk_ld, float* topk_scores, void* stream) {
+  MISA_REQUIRE(scores && row_len && tau && seg_cnt && cand_scores && cand_idx && cand_count && topk, "null pointer");
+  MISA_REQUIRE(k >= 1 && topk_ld >= k && n_rows >= 1 && max_len >= 1 && max_len <= ld, "bad arguments");
+  MISA_REQUIRE(cap >= 2 * k && cap <= 16384, "candidate capacity must lie in [2k, 16384]");
+  cudaStream_t st = as_stream(stream);
+  const int stride = (int)std::max<int64_t>(32, (max_len + 16383) / 16384);  // <= 16384 samples per row
+  const int64_t m = (max_len + stride - 1) / stride;
+  // tau: ~2k of the row's keys pass; rows with n <= cap keep every key
+  MISA_REQUIRE(beta >= 1.0f, "beta must be >= 1");
+  int rc = dispatch_capacity<ThresholdStepL>(m, st, scores, ld, row_len, n_rows, stride, k, beta, (int64_t)cap, tau);
+  MISA_REQUIRE(rc != -100, "long-row sample exceeds the register selector (max_len %lld)", (long long)max_len);
+  if (rc) return rc;
+  const int n_seg = (int)((max_len + kSeg - 1) / kSeg);
+  dim3 grid(n_seg, (unsigned)n_rows);
+  seg_count_kernel<<<grid, kSegThreads, 0, st>>>(scores, ld, row_len, tau, seg_cnt, n_seg);
+  MISA_LAUNCH_CHECK();
+  seg_compact_kernel<<<grid, kSegThreads, 0, st>>>(scores, ld, row_len, tau, seg_cnt, n_seg, cand_scores, cand_idx,
+                                                   cap, cand_count);
+  MISA_LAUNCH_CHECK();
+  rc = misa_select_dense_clamped(cand_scores, cap, cand_idx, cap, cand_count, n_rows, k, topk, topk_ld, topk_scores,
+                                 st);
+  if (rc) return rc;
+  seg_fixup_kernel<<<(unsigned)n_rows, kGlbThreads, 0, st>>>(scores, ld, row_len, cand_count, cap, k, topk, topk_ld,
+                                                             topk_scores);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
 }

@@ -450,8 +450,21 @@ class IndexerEngine:
         rows = self.dense_scores(x, heads, hq)
         tgt = out if self.method != "misa_hier" else self._buf("hier_cand", (x.T, kk), torch.int32, dev)
         self._mark("decode:select")
-        _lib.call("misa_select_dense", _ptr(rows), x.L, None, 0, _ptr(x.prefix), None, x.T, kk, _ptr(tgt),
-                  tgt.stride(0), None, self._stream())
+        if x.L <= 16384:  # the whole row fits the register selector
+            _lib.call("misa_select_dense", _ptr(rows), x.L, None, 0, _ptr(x.prefix), None, x.T, kk, _ptr(tgt),
+                      tgt.stride(0), None, self._stream())
+        else:
+            beta = 2.0 if kk < 4096 else 1.3
+            cap = min(16384, max(2 * kk, 1 << (int(math.ceil(1.5 * beta * kk)) - 1).bit_length()))
+            n_seg = -(-x.L // 4096)
+            tau = self._buf("long_tau", (x.T,), torch.float32, dev)
+            seg = self._buf("long_seg", (x.T, n_seg), torch.int32, dev)
+            cs = self._buf("long_cs", (x.T, cap), torch.float32, dev)
+            ci = self._buf("long_ci", (x.T, cap), torch.int32, dev)
+            cc = self._buf("long_cc", (x.T,), torch.int32, dev)
+            _lib.call("misa_select_dense_long", _ptr(rows), x.L, _ptr(x.prefix), x.T, kk, int(x.prefix_host.max()),
+                      float(beta), _ptr(tau), _ptr(seg), _ptr(cs), _ptr(ci), _ptr(cc), cap, _ptr(tgt), tgt.stride(0),
+                      None, self._stream())
         self._mark("decode:end")
         self.last_fallback_rows = 0
         h = min(self.h, x.H)

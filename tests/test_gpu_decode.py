@@ -70,3 +70,36 @@ def test_pooled_key_cache_decode_equals_full_recompute():
     torch.cuda.synchronize()
     assert cache.length == L
     assert torch.equal(a.heads, b.heads) and torch.equal(a.topk, b.topk)
+
+
+@pytest.mark.parametrize("quantize", [False, True])
+def test_dense_long_selector_matches_sort(quantize):
+    """misa_select_dense_long on long rows (incl. heavy ties -> on-device exact re-selection)
+    equals a (score desc, index asc) sort."""
+    from paper_2605_07363_b200 import _lib
+    torch.manual_seed(11)
+    T, L, k = 6, 50000, 700
+    s = torch.randn(T, L, device="cuda")
+    if quantize:
+        s = (s * 2).round() / 2  # few distinct values: ties at the cut, candidate overflow
+    n = torch.tensor([L, L - 1, 4000, 701, 700, 30000], dtype=torch.int32, device="cuda")
+    cap = 2048
+    n_seg = -(-L // 4096)
+    bufs = dict(tau=torch.empty(T, device="cuda"), seg=torch.empty(T, n_seg, dtype=torch.int32, device="cuda"),
+                cs=torch.empty(T, cap, device="cuda"), ci=torch.empty(T, cap, dtype=torch.int32, device="cuda"),
+                cc=torch.empty(T, dtype=torch.int32, device="cuda"))
+    out = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    outs = torch.empty(T, k, device="cuda")
+    _lib.call("misa_select_dense_long", s.data_ptr(), L, n.data_ptr(), T, k, L, 2.0, bufs["tau"].data_ptr(),
+              bufs["seg"].data_ptr(), bufs["cs"].data_ptr(), bufs["ci"].data_ptr(), bufs["cc"].data_ptr(), cap,
+              out.data_ptr(), k, outs.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    sc = s.cpu().numpy()
+    for r in range(T):
+        m = int(n[r])
+        order = np.lexsort((np.arange(m), -sc[r, :m]))[: min(k, m)]
+        exp = np.sort(order)
+        got = out[r].cpu().numpy()
+        assert got[: len(exp)].tolist() == exp.tolist(), r
+        assert (got[len(exp):] == -1).all()
+        np.testing.assert_array_equal(outs[r, : len(exp)].cpu().numpy(), sc[r, exp])
