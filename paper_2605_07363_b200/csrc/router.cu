@@ -295,9 +295,9 @@ __global__ void route_select_kernel(const float* __restrict__ partial, int n_chu
       } else {
         float s = 0.f;
         for (int c = 0; c < nch && c < n_chunks; ++c) s += partial[((int64_t)c * T + t) * Hp + j];
-        e = fabsf(wj) * s / (float)M;
+        e = M > 0 ? fabsf(wj) * s / (float)M : 0.f;
       }
-      v[r] = e;
+      v[r] = e != e ? -INFINITY : e;  // NaN never wins (and never breaks the argmax)
       if (importance) importance[(int64_t)t * Hp + j] = e;
     }
   }
@@ -322,7 +322,7 @@ __global__ void route_select_kernel(const float* __restrict__ partial, int n_chu
         bj = oj;
       }
     }
-    if ((bj & 31) == lane) taken[bj >> 5] = true;
+    if (bj != 0x7fffffff && (bj & 31) == lane) taken[(bj >> 5) & 3] = true;
   }
   int base = 0;
 #pragma unroll

@@ -439,6 +439,12 @@ class IndexerEngine:
         if prefix_len is None:
             prefix_len = np.full(Tq, L, dtype=np.int64)
         x = prepare_inputs(keys, queries, weights, prefix_len)
+        return self.decode_prepared(x, cache=cache, need_importance=need_importance, out=out)
+
+    def decode_prepared(self, x: PreparedInputs, *, cache=None, need_importance: bool = False,
+                        out: torch.Tensor | None = None) -> IndexerOutput:
+        """decode() on prepared inputs: no host synchronisation and no allocation once the
+        workspace exists, so it can be captured in a CUDA graph (``DecodeGraph``)."""
         dev = x.keys.device
         k = self.k
         if out is None:
@@ -506,3 +512,58 @@ class IndexerEngine:
         self.last_fallback_rows = nfb
         return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H],
                              candidates=cand, n_fallback_rows=nfb)
+
+
+class DecodeGraph:
+    """Per-token decode step replayed from a CUDA graph (serving path for configs C5).
+
+    The step (router on the cache's pooled state, key-split scoring, long-row exact
+    selection) is captured once per key bucket: work lists cover the cache length
+    rounded up to ``bucket`` keys while the kernels read the true prefix length from a
+    device buffer, so a graph serves every length in its bucket (the masked tail costs
+    < bucket keys) and is re-captured only when the cache crosses into the next bucket.
+    Inputs are copied into static buffers; the result tensor is reused across steps."""
+
+    def __init__(self, engine: "IndexerEngine", cache, n_rows: int, n_heads: int, bucket: int = 4096):
+        self.engine, self.cache, self.T, self.H = engine, cache, int(n_rows), int(n_heads)
+        self.bucket = check_positive_int(bucket, "bucket")
+        dev = cache.keys.device
+        self.Hp = heads_pad(self.H)
+        self.q = torch.zeros(self.T, self.Hp, cache.D, dtype=torch.bfloat16, device=dev)
+        self.w = torch.zeros(self.T, self.Hp, dtype=torch.float32, device=dev)
+        self.prefix = torch.zeros(self.T, dtype=torch.int32, device=dev)
+        self.out = torch.empty(self.T, engine.k, dtype=torch.int32, device=dev)
+        self.graph = None
+        self.Lb = 0
+        self.result = None
+
+    def _capture(self, Lb: int) -> None:
+        c = self.cache
+        x = PreparedInputs(c.keys[:Lb], self.q, self.w, self.prefix, np.full(self.T, Lb, dtype=np.int64), Lb,
+                           self.T, self.H, self.Hp, c.d, c.D, ("decode", Lb, self.T))
+        eng = self.engine
+        self.prefix.fill_(max(1, min(c.length, Lb)))  # warm-up on a valid prefix
+        stream = torch.cuda.Stream()
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            eng.decode_prepared(x, cache=c, out=self.out)  # warm-up: workspace + work lists
+        torch.cuda.current_stream().wait_stream(stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            self.result = eng.decode_prepared(x, cache=c, out=self.out)
+        self.graph, self.Lb = g, Lb
+
+    def step(self, queries, weights) -> IndexerOutput:
+        """Top-k of ``queries`` (T, H, d) / ``weights`` (T, H) against the whole cache."""
+        L = self.cache.length
+        if L < 1:
+            raise ValueError("empty cache")
+        Lb = min(self.cache.capacity, -(-L // self.bucket) * self.bucket)
+        if self.graph is None or Lb != self.Lb:
+            self._capture(Lb)
+        self.q[:, :self.H, :self.cache.d].copy_(queries, non_blocking=True)
+        self.w[:, :self.H].copy_(weights, non_blocking=True)
+        self.prefix.fill_(L)
+        self.graph.replay()
+        return self.result

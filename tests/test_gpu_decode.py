@@ -103,3 +103,28 @@ def test_dense_long_selector_matches_sort(quantize):
         assert got[: len(exp)].tolist() == exp.tolist(), r
         assert (got[len(exp):] == -1).all()
         np.testing.assert_array_equal(outs[r, : len(exp)].cpu().numpy(), sc[r, exp])
+
+
+@pytest.mark.parametrize("method", ["misa", "dsa"])
+def test_decode_graph_replay_matches_eager(method):
+    """DecodeGraph (CUDA-graph replay, bucketed work lists, device prefix length) == eager
+    decode, token after token, across a bucket boundary (re-capture)."""
+    from paper_2605_07363_b200 import DecodeGraph, IndexerEngine
+    from paper_2605_07363_b200.pooling import PooledKeyCache
+    L0, T, k, B = 20000, 4, 256, 1024
+    K, Q, W = _inputs(L0 + 600, T * 3, seed=13)
+    cache = PooledKeyCache(128, B, capacity=32768)
+    cache.append(K[:L0])
+    eng_g = IndexerEngine(method, budget_k=k, active_heads_h=8, block_size=B)
+    dg = DecodeGraph(eng_g, cache, T, 64, bucket=4096)
+    for step, L in enumerate((L0, L0 + 300, L0 + 600)):  # 20000 -> bucket 20480; 20600 -> 24576
+        if cache.length < L:
+            cache.append(K[cache.length:L])
+        q, w = Q[step * T:(step + 1) * T], W[step * T:(step + 1) * T]
+        got = dg.step(q, w)
+        ref = IndexerEngine(method, budget_k=k, active_heads_h=8, block_size=B).decode(queries=q, weights=w,
+                                                                                       cache=cache)
+        torch.cuda.synchronize()
+        assert torch.equal(got.topk, ref.topk), (method, L)
+        if method != "dsa":
+            assert torch.equal(got.heads, ref.heads)
