@@ -57,6 +57,7 @@ def _args():
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--hier", action="store_true", help="also time MISA-dagger (k'=--kprime)")
+    p.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
     return p.parse_args()
 
 
@@ -365,6 +366,14 @@ def run_ours(a):
                          f"(pool+route+score+top-k, fast32) in {cores} single-BLAS-thread processes "
                          f"({info['cpu_s']:.1f} s CPU), extrapolated linearly in prefix length to all {T} rows"}
 
+    decode = None
+    if world == 1 and not a.no_decode:
+        sys.path.insert(0, os.path.join(REPO, "tools"))
+        from decode_bench import decode_numbers
+        decode = {"what": "per-token decode step (C5 shapes): T query rows vs a PooledKeyCache of L keys, "
+                          "eager engine.decode and CUDA-graph DecodeGraph replay, ms per step",
+                  "rows": decode_numbers()}
+
     line = {
         "metric": METRIC, "value": round(misa_ms, 3), "unit": "ms/layer", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(misa_ms, 3), "higher_is_better": False,
@@ -381,6 +390,7 @@ def run_ours(a):
         "dsa_stages_ms": {k: round(v, 4) for k, v in dstages.items()},
         "fallback_rows": fallback,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
+        "decode": decode,
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)

@@ -997,7 +997,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk5_kernel(const ui
     }
     const int cq = min(max(c[q], 0), cap);
     // slot rows of this warp that can hold list elements (warp-uniform)
-    const int rv = min(EPT, max(0, (cq - (w % WPL) * WE + 31) >> 5));
+    const int rv = EPT;  // unguarded: predicated slots pipeline better than per-row branches
     ptx::mbar_wait(&mbar, phase);
     phase ^= 1;
     SEL_MARK(ti_, 1);
