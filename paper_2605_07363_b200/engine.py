@@ -420,6 +420,29 @@ class IndexerEngine:
                   _ptr(rows), x.L, self._stream())
         return rows
 
+    def dense_select(self, x: PreparedInputs, heads, hq: int, k: int, out: torch.Tensor,
+                     scores: torch.Tensor | None = None) -> None:
+        """Key-split dense scoring + exact per-row top-k (decode rows); ``scores`` (T, k)
+        receives the selected scores (a key shard's local top-k)."""
+        dev = x.keys.device
+        rows = self.dense_scores(x, heads, hq)
+        self._mark("decode:select")
+        if x.L <= 16384:  # the whole row fits the register selector
+            _lib.call("misa_select_dense", _ptr(rows), x.L, None, 0, _ptr(x.prefix), None, x.T, k, _ptr(out),
+                      out.stride(0), _ptr(scores), self._stream())
+            return
+        beta = 2.0 if k < 4096 else 1.3
+        cap = min(16384, max(2 * k, 1 << (int(math.ceil(1.5 * beta * k)) - 1).bit_length()))
+        n_seg = -(-x.L // 4096)
+        tau = self._buf("long_tau", (x.T,), torch.float32, dev)
+        seg = self._buf("long_seg", (x.T, n_seg), torch.int32, dev)
+        cs = self._buf("long_cs", (x.T, cap), torch.float32, dev)
+        ci = self._buf("long_ci", (x.T, cap), torch.int32, dev)
+        cc = self._buf("long_cc", (x.T,), torch.int32, dev)
+        _lib.call("misa_select_dense_long", _ptr(rows), x.L, _ptr(x.prefix), x.T, k, int(x.prefix_host.max()),
+                  float(beta), _ptr(tau), _ptr(seg), _ptr(cs), _ptr(ci), _ptr(cc), cap, _ptr(out), out.stride(0),
+                  _ptr(scores), self._stream())
+
     def decode(self, keys=None, queries=None, weights=None, prefix_len=None, *, cache=None,
                need_importance: bool = False, out: torch.Tensor | None = None) -> IndexerOutput:
         """Decode step: a few query rows (T <= a few hundred) against long prefixes.
@@ -453,24 +476,8 @@ class IndexerEngine:
         if self.method != "dsa":
             heads, hq, imp = self.route(x, need_importance, cache=cache)
         kk = k if self.method != "misa_hier" else max(self.kprime, k)
-        rows = self.dense_scores(x, heads, hq)
         tgt = out if self.method != "misa_hier" else self._buf("hier_cand", (x.T, kk), torch.int32, dev)
-        self._mark("decode:select")
-        if x.L <= 16384:  # the whole row fits the register selector
-            _lib.call("misa_select_dense", _ptr(rows), x.L, None, 0, _ptr(x.prefix), None, x.T, kk, _ptr(tgt),
-                      tgt.stride(0), None, self._stream())
-        else:
-            beta = 2.0 if kk < 4096 else 1.3
-            cap = min(16384, max(2 * kk, 1 << (int(math.ceil(1.5 * beta * kk)) - 1).bit_length()))
-            n_seg = -(-x.L // 4096)
-            tau = self._buf("long_tau", (x.T,), torch.float32, dev)
-            seg = self._buf("long_seg", (x.T, n_seg), torch.int32, dev)
-            cs = self._buf("long_cs", (x.T, cap), torch.float32, dev)
-            ci = self._buf("long_ci", (x.T, cap), torch.int32, dev)
-            cc = self._buf("long_cc", (x.T,), torch.int32, dev)
-            _lib.call("misa_select_dense_long", _ptr(rows), x.L, _ptr(x.prefix), x.T, kk, int(x.prefix_host.max()),
-                      float(beta), _ptr(tau), _ptr(seg), _ptr(cs), _ptr(ci), _ptr(cc), cap, _ptr(tgt), tgt.stride(0),
-                      None, self._stream())
+        self.dense_select(x, heads, hq, kk, tgt)
         self._mark("decode:end")
         self.last_fallback_rows = 0
         h = min(self.h, x.H)

@@ -17,7 +17,9 @@ rank b mod G), which keeps pooled blocks whole and balances causal prefill
      per-part top-k's.
 
 Rows come out row-sliced (rank r owns rows [r*T/G, (r+1)*T/G)); ``gather=True``
-all-gathers them.  The key cache is replicated here so that routing and the
+all-gathers them.  Decode (a few rows against long prefixes, ``decode``) routes every
+row locally (tiny), scores the shard with the key-split decode path, and one
+all-gather of the (T x k) local lists lets every rank merge every row.  The key cache is replicated here so that routing and the
 partial-block pooling need no extra exchange; only the scoring work is sharded.
 MISA-dagger is not sharded in this version.
 """
@@ -95,6 +97,21 @@ def exchange_by_rows(idx: torch.Tensor, scores: torch.Tensor, world: int, group=
     return torch.stack([g[sl] for g in gi]), torch.stack([g[sl] for g in gs])
 
 
+def gather_lists(idx: torch.Tensor, scores: torch.Tensor, world: int, group=None):
+    """(T, k) local lists on every rank -> (world, T, k) lists of every rank (decode exchange)."""
+    if world == 1:
+        return idx[None], scores[None]
+    gi = torch.empty((world,) + tuple(idx.shape), dtype=idx.dtype, device=idx.device)
+    gs = torch.empty((world,) + tuple(scores.shape), dtype=scores.dtype, device=scores.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gi, idx.contiguous(), group=group)
+        dist.all_gather_into_tensor(gs, scores.contiguous(), group=group)
+    else:
+        dist.all_gather(list(gi.unbind(0)), idx.contiguous(), group=group)
+        dist.all_gather(list(gs.unbind(0)), scores.contiguous(), group=group)
+    return gi, gs
+
+
 class ShardedIndexer:
     """Key-sharded DSA / MISA indexer for one rank of a ``torch.distributed`` group."""
 
@@ -163,4 +180,37 @@ class ShardedIndexer:
             else:
                 full.copy_(out)
             return full[: x.T]
+        return out
+
+    def decode(self, keys, queries, weights, prefix_len=None, *, cache=None):
+        """Decode step, key-sharded: every rank returns the global top-k of every row.
+
+        ``keys`` / ``cache`` hold the replicated key set (the router needs every pooled
+        block); each rank scores only its block-cyclic shard."""
+        if cache is not None:
+            keys = cache.keys[:cache.length, :cache.d]
+        G, r, k = self.world, self.rank, self.k
+        Tq, L = int(queries.shape[0]), int(keys.shape[0])
+        if prefix_len is None:
+            prefix_len = np.full(Tq, L, dtype=np.int64)
+        x = prepare_inputs(keys, queries, weights, prefix_len)
+        dev = x.keys.device
+        stream = torch.cuda.current_stream().cuda_stream
+        eng = self.engine
+        heads, hq = None, x.Hp
+        if self.method == "misa":
+            heads, hq, _ = eng.route(x, cache=cache)
+        n_loc = self.layout.local_count(x.prefix_host)
+        K_loc = self._local_keys(x)
+        xl = PreparedInputs(K_loc, x.queries, x.weights, torch.from_numpy(n_loc.astype(np.int32)).to(dev), n_loc,
+                            K_loc.shape[0], x.T, x.H, x.Hp, x.d, x.D, None)
+        loc_i = torch.full((x.T, k), -1, dtype=torch.int32, device=dev)
+        loc_s = torch.full((x.T, k), float("-inf"), dtype=torch.float32, device=dev)
+        if K_loc.shape[0] > 0:
+            eng.dense_select(xl, heads, hq, k, loc_i, scores=loc_s)
+        _lib.call("misa_shard_map_indices", loc_i.data_ptr(), loc_i.numel(), self.layout.block, G, r, stream)
+        parts_i, parts_s = gather_lists(loc_i, loc_s, G, self.group)
+        out = torch.empty((x.T, k), dtype=torch.int32, device=dev)
+        _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, x.T * k, x.T, k, k, out.data_ptr(), k,
+                  stream)
         return out

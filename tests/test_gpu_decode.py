@@ -128,3 +128,38 @@ def test_decode_graph_replay_matches_eager(method):
         assert torch.equal(got.topk, ref.topk), (method, L)
         if method != "dsa":
             assert torch.equal(got.heads, ref.heads)
+
+
+@pytest.mark.parametrize("method,G", [("misa", 2), ("misa", 8), ("dsa", 4)])
+def test_virtual_key_shards_decode_merge_to_single_gpu(method, G):
+    """G key shards on one GPU: per-shard decode top-k with scores -> global index map ->
+    merge == the unsharded decode (the ShardedIndexer.decode pipeline minus NCCL)."""
+    from paper_2605_07363_b200 import IndexerEngine, _lib, prepare_inputs
+    from paper_2605_07363_b200.engine import PreparedInputs
+    from paper_2605_07363_b200.sharded import KeyShardLayout
+    L, T, k, B = 70000, 6, 512, 1024
+    K, Q, W = _inputs(L, T, seed=17)
+    eng = IndexerEngine(method, budget_k=k, active_heads_h=8, block_size=B)
+    ref = eng.decode(K, Q, W)
+    x = prepare_inputs(K, Q, W, np.full(T, L))
+    heads, hq = (None, x.Hp)
+    if method == "misa":
+        heads, hq, _ = eng.route(x)
+        heads = heads.clone()
+    parts_i = torch.full((G, T, k), -1, dtype=torch.int32, device="cuda")
+    parts_s = torch.full((G, T, k), float("-inf"), device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for r in range(G):
+        lay = KeyShardLayout(G, r, B)
+        loc = torch.from_numpy(lay.local_keys(L)).cuda()
+        n_loc = lay.local_count(x.prefix_host)
+        Kl = x.keys.index_select(0, loc).contiguous()
+        xl = PreparedInputs(Kl, x.queries, x.weights, torch.from_numpy(n_loc.astype(np.int32)).cuda(), n_loc,
+                            Kl.shape[0], x.T, x.H, x.Hp, x.d, x.D, None)
+        IndexerEngine(method, budget_k=k, active_heads_h=8, block_size=B).dense_select(
+            xl, heads, hq, k, parts_i[r], scores=parts_s[r])
+        _lib.call("misa_shard_map_indices", parts_i[r].data_ptr(), parts_i[r].numel(), B, G, r, stream)
+    out = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, T * k, T, k, k, out.data_ptr(), k, stream)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref.topk)

@@ -100,3 +100,50 @@ def test_gloo_sharded_exchange_and_merge_equal_dense(world):
     for p in procs:
         p.join(timeout=60)
     assert all(res.values()), res
+
+
+def _decode_worker(rank, world, port, L, H, d, k, B, q):
+    """Decode exchange: every rank all-gathers the (T, k) local lists and merges every row."""
+    from paper_2605_07363_b200.sharded import gather_lists
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        K, Q, W = O.synthetic_prefill(91, L, H, d)
+        T = 5
+        rows = np.arange(L - T, L)  # decode rows see (almost) the whole prefix
+        lay = KeyShardLayout(world, rank, B)
+        loc = lay.local_keys(L)
+        li = np.full((T, k), -1, np.int64)
+        ls = np.full((T, k), -np.inf)
+        for j, t in enumerate(rows):
+            n_loc = int(lay.local_count(t + 1))
+            if n_loc == 0:
+                continue
+            sc = O.gated_relu_scores(K[loc[:n_loc]], Q[t], W[t], "fast32")
+            sel = O.topk_tokens(sc, k)
+            li[j, : sel.shape[0]] = lay.to_global(sel)
+            ls[j, : sel.shape[0]] = sc[sel]
+        gi, gs = gather_lists(torch.from_numpy(li), torch.from_numpy(ls), world)
+        got = _merge_np(gi.numpy(), gs.numpy(), k)
+        ok = True
+        for j, t in enumerate(rows):
+            ref = O.dsa_select(K[: t + 1], Q[t], W[t], k, "fast32")["selection"]
+            row = got[j][got[j] >= 0]
+            ok &= row.tolist() == ref.tolist()
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_sharded_decode_gather_and_merge_equal_dense():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world, L, H, d, k, B = 2, 400, 8, 16, 24, 16
+    port = _free_port()
+    procs = [ctx.Process(target=_decode_worker, args=(r, world, port, L, H, d, k, B, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()), res
