@@ -307,6 +307,22 @@ def run_ours(a):
         e2e = {"value": e2e_ms, "unit": "ms/layer", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(T * a.k * 4)}
 
+    # --- C5: key-sharded decode step at 1M keys (all ranks; max over ranks)
+    sdec = None
+    if world > 1 and not a.no_decode:
+        from paper_2605_07363_b200.sharded import ShardedIndexer
+        Ld, Td = 1 << 20, 64
+        g2 = torch.Generator(device="cuda").manual_seed(1)
+        Kd = torch.randn(Ld, a.d, device="cuda", generator=g2).bfloat16()
+        Qd = torch.randn(Td, a.H, a.d, device="cuda", generator=g2).bfloat16()
+        Wd = torch.softmax(torch.randn(Td, a.H, device="cuda", generator=g2), -1).float()
+        sd = ShardedIndexer("misa", world=world, rank=rank, budget_k=a.k, active_heads_h=a.h, block_size=a.B)
+        dms = max_over_ranks(_time_steps(lambda: sd.decode(Kd, Qd, Wd), 10, 3, barrier))
+        sdec = {"method": "misa", "L": Ld, "T": Td, "ms_per_step": round(dms, 4),
+                "what": "key-sharded decode step: local key-split scoring + long-row top-k with scores, "
+                        "NCCL all-gather of the row lists, merge on every rank"}
+        del Kd, Qd, Wd
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -390,7 +406,7 @@ def run_ours(a):
         "dsa_stages_ms": {k: round(v, 4) for k, v in dstages.items()},
         "fallback_rows": fallback,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
-        "decode": decode,
+        "decode": decode, "sharded_decode": sdec,
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)
