@@ -1,0 +1,46 @@
+"""Two ranks sharing one GPU over gloo (the box has 1 GPU): ShardedIndexer.run / .decode
+must equal the single-GPU engine.  Dev check for the multi-GPU host path."""
+import os, sys, socket
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_07363_b200 import IndexerEngine
+    from paper_2605_07363_b200.sharded import ShardedIndexer
+    g = torch.Generator(device="cuda").manual_seed(0)
+    L, H, d, k, B = 20000, 64, 128, 512, 1024
+    K = torch.randn(L, d, device="cuda", generator=g).bfloat16()
+    Q = torch.randn(L, H, d, device="cuda", generator=g).bfloat16()
+    W = torch.softmax(torch.randn(L, H, device="cuda", generator=g), -1).float()
+    ok = {}
+    for m in ("misa", "dsa"):
+        ref = IndexerEngine(m, budget_k=k, active_heads_h=8, block_size=B).run(K, Q, W).topk
+        got = ShardedIndexer(m, world=world, rank=rank, budget_k=k, active_heads_h=8, block_size=B).run(
+            K, Q, W, gather=True)
+        ok[m + "_prefill"] = bool(torch.equal(got, ref))
+        Qd, Wd = Q[-8:].contiguous(), W[-8:].contiguous()
+        refd = IndexerEngine(m, budget_k=k, active_heads_h=8, block_size=B).decode(K, Qd, Wd).topk
+        gotd = ShardedIndexer(m, world=world, rank=rank, budget_k=k, active_heads_h=8, block_size=B).decode(K, Qd, Wd)
+        ok[m + "_decode"] = bool(torch.equal(gotd, refd))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    [p.start() for p in ps]
+    res = dict(q.get(timeout=600) for _ in range(2))
+    [p.join() for p in ps]
+    print(res)
+    assert all(all(v.values()) for v in res.values()), res
+    print("sharded smoke ok")
