@@ -21,7 +21,8 @@ all-gathers them.  Decode (a few rows against long prefixes, ``decode``) routes 
 row locally (tiny), scores the shard with the key-split decode path, and one
 all-gather of the (T x k) local lists lets every rank merge every row.  The key cache is replicated here so that routing and the
 partial-block pooling need no extra exchange; only the scoring work is sharded.
-MISA-dagger is not sharded in this version.
+MISA-dagger: the coarse top-k' is sharded and merged like the top-k; each rank then
+re-ranks its own rows' merged candidates against the (replicated) key set.
 """
 
 from __future__ import annotations
@@ -117,13 +118,16 @@ class ShardedIndexer:
 
     def __init__(self, method: str = "misa", *, world: int, rank: int, group=None, shard_block: int | None = None,
                  **engine_kwargs):
-        if method not in ("dsa", "misa"):
-            raise ValueError(f"sharded execution supports 'dsa' and 'misa', got {method!r}")
+        if method not in ("dsa", "misa", "misa_hier"):
+            raise ValueError(f"sharded execution supports 'dsa', 'misa' and 'misa_hier', got {method!r}")
         self.method = method
         self.world, self.rank, self.group = world, rank, group
         self.engine = IndexerEngine(method, **engine_kwargs)
         self.layout = KeyShardLayout(world, rank, shard_block or self.engine.B)
         self.k = self.engine.k
+        kc = self.k if method != "misa_hier" else max(self.engine.kprime, self.k)
+        if world * kc > 16384:  # misa_merge_topk holds the union of the per-rank lists in registers
+            raise ValueError(f"world_size * candidate budget = {world * kc} exceeds the merge capacity (16384)")
         self._cache: dict = {}
         self.last_fallback_rows = 0
 
@@ -144,8 +148,8 @@ class ShardedIndexer:
         stream = torch.cuda.current_stream().cuda_stream
 
         heads, hq = None, x.Hp
-        if self.method == "misa":
-            r0, r1 = min(x.T, r * per), min(x.T, (r + 1) * per)
+        r0, r1 = min(x.T, r * per), min(x.T, (r + 1) * per)
+        if self.method != "dsa":
             xs = PreparedInputs(x.keys, x.queries[r0:r1], x.weights[r0:r1], x.prefix[r0:r1], x.prefix_host[r0:r1],
                                 x.L, r1 - r0, x.H, x.Hp, x.d, x.D, None)
             h_loc, hq, _ = self.engine.route(xs) if r1 > r0 else (None, 8, None)
@@ -164,15 +168,25 @@ class ShardedIndexer:
         K_loc = self._local_keys(x)
         xl = PreparedInputs(K_loc, x.queries, x.weights, torch.from_numpy(n_loc.astype(np.int32)).to(dev), n_loc,
                             K_loc.shape[0], x.T, x.H, x.Hp, x.d, x.D, None)
-        loc_i = torch.full((T_pad, k), -1, dtype=torch.int32, device=dev)
-        loc_s = torch.full((T_pad, k), float("-inf"), dtype=torch.float32, device=dev)
-        self.last_fallback_rows = self.engine.select(xl, heads, hq, k, loc_i[: x.T], tag="shard", scores=loc_s[: x.T])
+        kc = k if self.method != "misa_hier" else max(self.engine.kprime, k)  # coarse budget
+        loc_i = torch.full((T_pad, kc), -1, dtype=torch.int32, device=dev)
+        loc_s = torch.full((T_pad, kc), float("-inf"), dtype=torch.float32, device=dev)
+        self.last_fallback_rows = self.engine.select(xl, heads, hq, kc, loc_i[: x.T], tag="shard",
+                                                     scores=loc_s[: x.T])
         _lib.call("misa_shard_map_indices", loc_i.data_ptr(), loc_i.numel(), self.layout.block, G, r, stream)
 
         parts_i, parts_s = exchange_by_rows(loc_i, loc_s, G, self.group)
-        out = torch.empty((per, k), dtype=torch.int32, device=dev)
-        _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, per * k, per, k, k, out.data_ptr(), k,
-                  stream)
+        merged = torch.empty((per, kc), dtype=torch.int32, device=dev)
+        _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, per * kc, per, kc, kc,
+                  merged.data_ptr(), kc, stream)
+        if self.method != "misa_hier":
+            out = merged
+        else:  # MISA-dagger fine stage on this rank's rows (dsa.py:95-115 on the merged candidates)
+            out = torch.full((per, k), -1, dtype=torch.int32, device=dev)
+            if r1 > r0:
+                xs = PreparedInputs(x.keys, x.queries[r0:r1], x.weights[r0:r1], x.prefix[r0:r1],
+                                    x.prefix_host[r0:r1], x.L, r1 - r0, x.H, x.Hp, x.d, x.D, None)
+                self.engine.refine(xs, merged[: r1 - r0], k, out[: r1 - r0])
         if gather:
             full = torch.empty((G * per, k), dtype=torch.int32, device=dev)
             if G > 1:
@@ -198,19 +212,24 @@ class ShardedIndexer:
         stream = torch.cuda.current_stream().cuda_stream
         eng = self.engine
         heads, hq = None, x.Hp
-        if self.method == "misa":
+        if self.method != "dsa":
             heads, hq, _ = eng.route(x, cache=cache)
+        kc = k if self.method != "misa_hier" else max(eng.kprime, k)
         n_loc = self.layout.local_count(x.prefix_host)
         K_loc = self._local_keys(x)
         xl = PreparedInputs(K_loc, x.queries, x.weights, torch.from_numpy(n_loc.astype(np.int32)).to(dev), n_loc,
                             K_loc.shape[0], x.T, x.H, x.Hp, x.d, x.D, None)
-        loc_i = torch.full((x.T, k), -1, dtype=torch.int32, device=dev)
-        loc_s = torch.full((x.T, k), float("-inf"), dtype=torch.float32, device=dev)
+        loc_i = torch.full((x.T, kc), -1, dtype=torch.int32, device=dev)
+        loc_s = torch.full((x.T, kc), float("-inf"), dtype=torch.float32, device=dev)
         if K_loc.shape[0] > 0:
-            eng.dense_select(xl, heads, hq, k, loc_i, scores=loc_s)
+            eng.dense_select(xl, heads, hq, kc, loc_i, scores=loc_s)
         _lib.call("misa_shard_map_indices", loc_i.data_ptr(), loc_i.numel(), self.layout.block, G, r, stream)
         parts_i, parts_s = gather_lists(loc_i, loc_s, G, self.group)
+        merged = torch.empty((x.T, kc), dtype=torch.int32, device=dev)
+        _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, x.T * kc, x.T, kc, kc,
+                  merged.data_ptr(), kc, stream)
+        if self.method != "misa_hier":
+            return merged
         out = torch.empty((x.T, k), dtype=torch.int32, device=dev)
-        _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, x.T * k, x.T, k, k, out.data_ptr(), k,
-                  stream)
+        eng.refine(x, merged, k, out)
         return out

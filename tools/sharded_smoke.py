@@ -20,14 +20,14 @@ def worker(rank, world, port, q):
     Q = torch.randn(L, H, d, device="cuda", generator=g).bfloat16()
     W = torch.softmax(torch.randn(L, H, device="cuda", generator=g), -1).float()
     ok = {}
-    for m in ("misa", "dsa"):
-        ref = IndexerEngine(m, budget_k=k, active_heads_h=8, block_size=B).run(K, Q, W).topk
-        got = ShardedIndexer(m, world=world, rank=rank, budget_k=k, active_heads_h=8, block_size=B).run(
-            K, Q, W, gather=True)
+    for m in ("misa", "dsa", "misa_hier"):
+        kw = dict(budget_k=k, active_heads_h=8, block_size=B, candidate_kprime=2048)
+        ref = IndexerEngine(m, **kw).run(K, Q, W).topk
+        got = ShardedIndexer(m, world=world, rank=rank, **kw).run(K, Q, W, gather=True)
         ok[m + "_prefill"] = bool(torch.equal(got, ref))
         Qd, Wd = Q[-8:].contiguous(), W[-8:].contiguous()
-        refd = IndexerEngine(m, budget_k=k, active_heads_h=8, block_size=B).decode(K, Qd, Wd).topk
-        gotd = ShardedIndexer(m, world=world, rank=rank, budget_k=k, active_heads_h=8, block_size=B).decode(K, Qd, Wd)
+        refd = IndexerEngine(m, **kw).decode(K, Qd, Wd).topk
+        gotd = ShardedIndexer(m, world=world, rank=rank, **kw).decode(K, Qd, Wd)
         ok[m + "_decode"] = bool(torch.equal(gotd, refd))
     q.put((rank, ok))
     dist.destroy_process_group()
