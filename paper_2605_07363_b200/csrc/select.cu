@@ -905,7 +905,7 @@ __device__ unsigned long long g_sel_trace[64][16];
 // with c % 4 == q, so all selected elements of a chunk are contiguous in one list and
 //   pos = #selected in chunks < c (block scan of a chunk histogram) + rank within c.
 template <int NT, int EPT>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk5_kernel(const uint64_t* __restrict__ cand,
+__global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_kernel(const uint64_t* __restrict__ cand,
                                                       const int32_t* __restrict__ cand_count, int cap,
                                                       const int32_t* __restrict__ prefix_len, int n_rows, int k,
                                                       int n_chunks, int32_t* __restrict__ topk, int64_t topk_ld,
@@ -1679,7 +1679,7 @@ static int launch_topk5(cudaStream_t st, const uint64_t* cand, const int32_t* cc
   // NT*EPT == 4*cap with cap a multiple of 32*EPT*(NT/128)
   if (cap == 256 * 8 / 4) return launch_topk5_t<256, 8>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
   if (cap == 256 * 16 / 4) return launch_topk5_t<256, 16>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
-  if (cap == 256 * 24 / 4) return launch_topk5_t<256, 24>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+  if (cap == 512 * 12 / 4) return launch_topk5_t<512, 12>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
   if (cap == 256 * 32 / 4) return launch_topk5_t<256, 32>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
   if (cap == 512 * 24 / 4) return launch_topk5_t<512, 24>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
   if (cap == 512 * 32 / 4) return launch_topk5_t<512, 32>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
