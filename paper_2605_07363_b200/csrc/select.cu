@@ -30,6 +30,36 @@
 
 namespace misa {
 
+// Optional phase trace (tools/sel_trace: built with -DMISA_SEL_TRACE, never in the product).
+#ifdef MISA_SEL_TRACE
+__device__ unsigned long long g_sel_trace[64][16];
+__device__ int g_sel_trace_row;
+#define SEL_MARK(row_i, ph)                                                   \
+  do {                                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (row_i) < 64) g_sel_trace[row_i][ph] = clock64(); \
+  } while (0)
+#else
+#define SEL_MARK(row_i, ph) \
+  do {                      \
+  } while (0)
+#endif
+
+
+#ifdef MISA_SEL_TRACE
+#define CUT_MARK(ph) SEL_MARK(g_sel_trace_row, ph)
+#define CUT_MARK_CB(v)                                                          \
+  do {                                                                          \
+    if (g_sel_trace_row < 64) g_sel_trace[g_sel_trace_row][15] = (unsigned long long)(v); \
+  } while (0)
+#else
+#define CUT_MARK(ph) \
+  do {               \
+  } while (0)
+#define CUT_MARK_CB(v) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr int kMaxLists = 8;
 
 template <int NT>
@@ -57,6 +87,33 @@ struct SelSh {
 };
 
 constexpr int kBucketMax = 256;
+
+// Cross-warp combines without serial smem chains: lane i reads warp i's value, then one
+// warp reduction / scan (NW <= 32).
+template <int NW>
+__device__ __forceinline__ int warps_exclusive(const int* vals, int w) {
+  const int lane = threadIdx.x & 31;
+  int v = lane < NW ? vals[lane] : 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  const int incl_prev = __shfl_sync(0xffffffffu, v, (w + 31) & 31);
+  return w == 0 ? 0 : incl_prev;  // inclusive sum of warps [0, w-1]
+}
+template <int NW>
+__device__ __forceinline__ uint32_t warps_min(const uint32_t* vals) {
+  const int lane = threadIdx.x & 31;
+  return __reduce_min_sync(0xffffffffu, lane < NW ? vals[lane] : 0xffffffffu);
+}
+template <int NW>
+__device__ __forceinline__ uint32_t warps_max(const uint32_t* vals) {
+  const int lane = threadIdx.x & 31;
+  return __reduce_max_sync(0xffffffffu, lane < NW ? vals[lane] : 0u);
+}
+
+
 
 // Warp-level: largest v with count(x >= v) >= j among this warp's values (x == 0: empty),
 // searching bits [hi, 0] on top of `prefix`.
@@ -496,7 +553,9 @@ __device__ void v3_cut(const uint32_t (&key)[EPT], const int32_t* sidx, int N, i
 // ranked exactly by (key desc, index asc) with one element per thread.
 template <int NT, int EPT, typename IdxFn>
 __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk, SelSh<NT>& sh, int& parity,
-                         uint32_t& v_out, int& thr_out, int rv = EPT) {
+                         uint32_t& v_out, int& thr_out, int rv = EPT, bool staged_minmax = false) {
+  // staged_minmax: the caller already zeroed sh.hist and published per-warp sh.rmin /
+  // sh.rmax behind a barrier (saves this function's first barrier)
   // rv: warp-uniform number of leading slot rows that can hold valid keys (rows >= rv
   // are skipped without issuing their instructions)
   constexpr int NW = NT / 32;
@@ -504,29 +563,27 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
   static_assert(NB % NT == 0 && BPT >= 1 && BPT <= 16, "bins per thread");
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   uint32_t mn = 0xffffffffu, mx = 0u;
+  if (!staged_minmax) {
 #pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    if (r < rv && key[r]) {
-      mn = min(mn, key[r]);
-      mx = max(mx, key[r]);
+    for (int r = 0; r < EPT; ++r) {
+      if (r < rv && key[r]) {
+        mn = min(mn, key[r]);
+        mx = max(mx, key[r]);
+      }
     }
-  }
-  mn = __reduce_min_sync(0xffffffffu, mn);
-  mx = __reduce_max_sync(0xffffffffu, mx);
-  if (lane == 0) {
-    sh.rmin[w] = mn;
-    sh.rmax[w] = mx;
-  }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) {
+      sh.rmin[w] = mn;
+      sh.rmax[w] = mx;
+    }
 #pragma unroll
-  for (int i = 0; i < BPT; ++i) sh.hist[tid * BPT + i] = 0u;
-  __syncthreads();
-  mn = sh.rmin[0];
-  mx = sh.rmax[0];
-#pragma unroll
-  for (int i = 1; i < NW; ++i) {
-    mn = min(mn, sh.rmin[i]);
-    mx = max(mx, sh.rmax[i]);
+    for (int i = 0; i < BPT; ++i) sh.hist[tid * BPT + i] = 0u;
+    __syncthreads();
   }
+  CUT_MARK(9);
+  mn = warps_min<NW>(sh.rmin);
+  mx = warps_max<NW>(sh.rmax);
   // level window: keys in [lo, lo + span) with span - 1 <= 0xffffffff, bins of 2^sft
   uint32_t lo = mn, span_m1 = mx - mn;
   int sft = span_m1 == 0u ? 0 : max(0, 32 - __clz(span_m1) - 11);
@@ -540,6 +597,7 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
       }
     }
     __syncthreads();
+    CUT_MARK(10);
     // thread tid owns bins [NB - BPT*(tid+1), NB - BPT*tid): descending key order
     uint32_t c[BPT];
     int tot = 0;
@@ -556,8 +614,7 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
     }
     if (lane == 31) sh.hscan[w] = incl;
     __syncthreads();
-    int above = incl - tot;
-    for (int i = 0; i < w; ++i) above += sh.hscan[i];
+    int above = incl - tot + warps_exclusive<NW>(sh.hscan, w);
     if (above < need && need <= above + tot) {
 #pragma unroll
       for (int i = 0; i < BPT; ++i) {
@@ -578,6 +635,7 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
     cB = sh.hb_count;
     lo += static_cast<uint32_t>(B) << sft;
     span_m1 = sft == 0 ? 0u : ((1u << sft) - 1u);
+    CUT_MARK(11);
     if (cB <= kBucketMax || sft == 0) break;
     sft = max(0, sft - 11);
   }
@@ -592,22 +650,26 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
       }
     }
     __syncthreads();
-    // exact rank of each boundary element under (key desc, index asc); the one with
-    // rank need-1 is the cut
-    for (int e = tid; e < cB; e += NT) {
+    CUT_MARK(12);
+    // exact rank of each boundary element under (key desc, index asc), one warp per
+    // element, lanes over the others; the element of rank need-1 is the cut
+    for (int e = w; e < cB; e += NW) {
       const uint32_t ke = sh.bkey[e];
       const int ie = sh.bidx[e];
       int rank = 0;
-      for (int f = 0; f < cB; ++f) {
+      for (int f = lane; f < cB; f += 32) {
         const uint32_t kf = sh.bkey[f];
         rank += (kf > ke) || (kf == ke && sh.bidx[f] < ie);
       }
-      if (rank == need - 1) {
+      rank = __reduce_add_sync(0xffffffffu, rank);
+      if (lane == 0 && rank == need - 1) {
         sh.res_v = ke;
         sh.res_thr = ie;
       }
     }
     __syncthreads();
+    CUT_MARK(13);
+    if (threadIdx.x == 0 && blockIdx.x == 0) CUT_MARK_CB(cB);
     v_out = sh.res_v;
     thr_out = sh.res_thr;
     __syncthreads();
@@ -644,8 +706,7 @@ __device__ void v3_select(const uint32_t (&key)[EPT], const int32_t* sidx, int N
   }
   if (lane == 0) sh.wtot[w] = cnt;
   __syncthreads();
-  int run = 0;
-  for (int i = 0; i < w; ++i) run += sh.wtot[i];
+  int run = warps_exclusive<NW>(sh.wtot, w);
   const uint32_t lt = ptx::lanemask_lt();
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
@@ -883,20 +944,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uin
   }
 }
 
-// Optional phase trace (tools/sel_trace: built with -DMISA_SEL_TRACE, never in the product).
-#ifdef MISA_SEL_TRACE
-__device__ unsigned long long g_sel_trace[64][16];
-#define SEL_MARK(row_i, ph)                                                   \
-  do {                                                                         \
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (row_i) < 64) g_sel_trace[row_i][ph] = clock64(); \
-  } while (0)
-#else
-#define SEL_MARK(row_i, ph) \
-  do {                      \
-  } while (0)
-#endif
-
-
 // ---------------------------------------------- v5 candidates -> top-k ----
 // Persistent, prefetching, merge-free.  Warp w owns slots of quadrant list
 // q = w / (NW/4) (NT*EPT == 4*cap, cap a multiple of 32*EPT), so extraction is one
@@ -918,20 +965,22 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
   __shared__ TopkPrefetch pf;
   uint64_t* raw = reinterpret_cast<uint64_t*>(dsm);                    // list q at raw + q*cap
   uint32_t* H = reinterpret_cast<uint32_t*>(raw + (size_t)kQuadrants * cap);  // chunk counts -> prefix
-  uint16_t* G0 = reinterpret_cast<uint16_t*>(H + n_chunks);             // first compacted rank of a chunk
-  int32_t* cidx = reinterpret_cast<int32_t*>(G0 + ((n_chunks + 7) & ~7));  // compacted indices
+  uint32_t* G0 = H + n_chunks;                                          // first compacted rank of a chunk
+  int32_t* cidx = reinterpret_cast<int32_t*>(G0 + n_chunks);            // compacted indices
   float* csc = reinterpret_cast<float*>(cidx + k);                       // compacted scores (optional)
   const bool want_scores = topk_scores != nullptr;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int q = w / WPL;                       // this warp's quadrant list
   const int i0 = (w % WPL) * WE + lane;        // list position of slot 0 (slot r: i0 + 32r)
 
-  int nx_n = 0, nx_c[kQuadrants] = {0, 0, 0, 0};
+  // (n, counts) of the row after next, loaded one row ahead of use into registers (one
+  // 16-byte load for the four counts; nothing waits on them until the next issue())
+  int nx_n = 0;
+  int4 nx_c4 = make_int4(0, 0, 0, 0);
   auto load_meta = [&](int row) {
     if (row < n_rows) {
-      nx_n = prefix_len[row];
-#pragma unroll
-      for (int j = 0; j < kQuadrants; ++j) nx_c[j] = cand_count[(int64_t)row * kQuadrants + j];
+      nx_n = __ldg(prefix_len + row);
+      nx_c4 = __ldg(reinterpret_cast<const int4*>(cand_count) + row);
     }
   };
   auto issue = [&](int row) {
@@ -939,17 +988,18 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     pf.copy = false;
     if (row >= n_rows) return;
     pf.n = nx_n;
+    const int nc[kQuadrants] = {nx_c4.x, nx_c4.y, nx_c4.z, nx_c4.w};
 #pragma unroll
-    for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nx_c[j];
+    for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nc[j];
     // no candidates needed: every prefix token (n <= k) or an empty prefix (counts unset)
     if ((nx_n <= k && !want_scores) || nx_n <= 0) return;
     uint32_t bytes = 0;
 #pragma unroll
-    for (int j = 0; j < kQuadrants; ++j) bytes += ((min(max(nx_c[j], 0), cap) * 8u) + 15u) & ~15u;
+    for (int j = 0; j < kQuadrants; ++j) bytes += ((min(max(nc[j], 0), cap) * 8u) + 15u) & ~15u;
     ptx::mbar_arrive_expect_tx(&mbar, bytes);
 #pragma unroll
     for (int j = 0; j < kQuadrants; ++j) {
-      const uint32_t b = ((min(max(nx_c[j], 0), cap) * 8u) + 15u) & ~15u;
+      const uint32_t b = ((min(max(nc[j], 0), cap) * 8u) + 15u) & ~15u;
       if (b) ptx::bulk_g2s(raw + (size_t)j * cap, cand + ((int64_t)row * kQuadrants + j) * cap, b, &mbar);
     }
     pf.copy = true;
@@ -961,11 +1011,17 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     issue(blockIdx.x);
     load_meta(blockIdx.x + gridDim.x);
   }
+  __syncthreads();  // mbarrier init and the first row's pf visible to every thread
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < n_rows; t += gridDim.x) {
-    __syncthreads();
+    // no barrier here: pf was written behind the previous row's barriers (or the prologue's;
+    // early-exit paths sync before leaving), and this row's first smem writes follow its
+    // extraction barrier
     const int ti_ = (t - blockIdx.x) / gridDim.x;
     (void)ti_;
+#ifdef MISA_SEL_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_trace_row = ti_;
+#endif
     SEL_MARK(ti_, 0);
     const int n = pf.n;
     const bool copy = pf.copy;
@@ -986,6 +1042,7 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
         if (outs) outs[i] = -INFINITY;
       }
       if (tid == 0 && flags) flags[t] = 0;
+      __syncthreads();  // pf (next row) published before anyone reads it
       continue;
     }
     bool overflow = false;
@@ -1003,6 +1060,7 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     SEL_MARK(ti_, 1);
     uint32_t key[EPT];
     int32_t idx[EPT];
+    uint32_t mn = 0xffffffffu, mx = 0u;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
       key[r] = 0u;
@@ -1012,8 +1070,20 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
         const uint2 rw = *reinterpret_cast<const uint2*>(raw + (size_t)q * cap + (i < cq ? i : 0));
         key[r] = i < cq ? float_key(__uint_as_float(rw.x)) : 0u;
         idx[r] = static_cast<int32_t>(rw.y);
+        if (i < cq) {
+          mn = min(mn, key[r]);
+          mx = max(mx, key[r]);
+        }
       }
     }
+    // the cut's first phase rides on this barrier: per-warp min / max and a zeroed histogram
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) {
+      sh.rmin[w] = mn;
+      sh.rmax[w] = mx;
+    }
+    for (int i = tid; i < 2048; i += NT) sh.hist[i] = 0u;
     __syncthreads();  // raw consumed: start the next row's copy
     SEL_MARK(ti_, 2);
     if (tid == 0) {
@@ -1023,13 +1093,15 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     if (overflow || total < kk) {
       for (int i = tid; i < k; i += NT) out[i] = -1;
       if (tid == 0 && flags) flags[t] = overflow ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
+      __syncthreads();  // pf (next row) published before anyone reads it
       continue;
     }
     // ---- cut: kk-th element under (score desc, index asc)
     uint32_t v = 0;
     int thr = 0x7fffffff;
     int parity = 0;
-    if (kk < total) hist_cut<NT, EPT>(key, [&](int r) { return idx[r]; }, total, kk, sh, parity, v, thr, rv);
+    if (kk < total)
+      hist_cut<NT, EPT>(key, [&](int r) { return idx[r]; }, total, kk, sh, parity, v, thr, rv, /*staged=*/true);
     SEL_MARK(ti_, 3);
     // ---- compaction of the selected elements (list-major order) into cidx / csc
     const int nch = (n + 31) >> 5;
@@ -1046,11 +1118,13 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
       }
     }
     if (lane == 0) sh.wtot[w] = cnt;
-    for (int i = tid; i < nch; i += NT) H[i] = 0u;
+    for (int i = tid; i < nch; i += NT) {
+      H[i] = 0u;
+      G0[i] = 0xffffffffu;
+    }
     __syncthreads();
     SEL_MARK(ti_, 4);
-    int run = 0;
-    for (int i = 0; i < w; ++i) run += sh.wtot[i];
+    int run = warps_exclusive<NW>(sh.wtot, w);
     const uint32_t lt = ptx::lanemask_lt();
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
@@ -1061,20 +1135,17 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
           const int g = run + __popc(bal & lt);
           cidx[g] = idx[r];
           if (want_scores) csc[g] = key_float(key[r]);
+          // a chunk's selected elements are contiguous in this order: count them and keep
+          // the smallest rank (the chunk's start)
+          const int ch = idx[r] >> 5;
+          atomicAdd(&H[ch], 1u);
+          atomicMin(&G0[ch], static_cast<uint32_t>(g));
         }
         run += __popc(bal);
       }
     }
     __syncthreads();
     SEL_MARK(ti_, 5);
-    // ---- chunk segments over the compacted elements (dense: no predicated slots);
-    // a chunk's elements are contiguous, its first one records its rank
-    for (int g = tid; g < kk; g += NT) {
-      const int ch = cidx[g] >> 5;
-      if (g == 0 || (cidx[g - 1] >> 5) != ch) G0[ch] = static_cast<uint16_t>(g);
-      atomicAdd(&H[ch], 1u);
-    }
-    __syncthreads();
     SEL_MARK(ti_, 6);
     // ---- exclusive scan of the chunk histogram (in place)
     {
@@ -1090,8 +1161,7 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
       }
       if (lane == 31) sh.hscan[w] = incl;
       __syncthreads();
-      int base = incl - s;
-      for (int i = 0; i < w; ++i) base += sh.hscan[i];
+      int base = incl - s + warps_exclusive<NW>(sh.hscan, w);
       for (int i = c0; i < c1; ++i) {
         const int h = static_cast<int>(H[i]);
         H[i] = static_cast<uint32_t>(base);
@@ -1658,8 +1728,7 @@ struct MergeL {
 template <int NT, int EPT>
 static int launch_topk5_t(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl,
                           int64_t T, int k, int n_chunks, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
-  const size_t bytes = (size_t)kQuadrants * cap * 8 + (size_t)n_chunks * 4 + (((size_t)n_chunks + 7) & ~size_t(7)) * 2 +
-                       (size_t)k * (ts ? 8 : 4);
+  const size_t bytes = (size_t)kQuadrants * cap * 8 + (size_t)n_chunks * 8 + (size_t)k * (ts ? 8 : 4);
   if (bytes > 200 * 1024) return -100;
   auto kern = topk5_kernel<NT, EPT>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));

@@ -39,3 +39,11 @@ print("rows", ok.sum(), "median cycles per phase:")
 for i, nm in enumerate(names[1:]):
     print(f"  {names[i]:>9s}->{nm:<9s} {int(np.median(d[ok, i])):8d}")
 print("  row total", int(np.median(a[ok, 8] - a[ok, 0])), " row-to-row", int(np.median(np.diff(a[ok, 0]))))
+cut = a[:, 9:14]
+okc = ok & (cut[:, 0] > 0) & (cut[:, 4] > 0)
+if okc.any():
+    seq = np.concatenate([a[:, 2:3], cut], 1)  # extract end -> cut marks
+    dd = np.diff(seq, axis=1)
+    for i, nm in enumerate(["minmax", "hist", "scan+lvl", "collect", "rank"]):
+        print(f"  cut:{nm:<9s} {int(np.median(dd[okc, i])):8d}")
+    print("  boundary bin sizes:", a[okc, 15][:20].tolist())
