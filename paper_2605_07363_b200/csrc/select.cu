@@ -315,7 +315,7 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int x) {
 // value and costs one atomic per sample and three barriers per row.  The kernel is
 // kept lean (registers, 9 KB smem) so that many rows are in flight per SM.
 template <int NT, int EPT>
-__global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__ s, int64_t ld,
+__global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kernel(const float* __restrict__ s, int64_t ld,
                                                        const int32_t* __restrict__ prefix_len, int stride, int k,
                                                        float beta, int64_t append_all, float* __restrict__ tau,
                                                        int elem_step = 1) {
@@ -334,18 +334,17 @@ __global__ void __launch_bounds__(NT) threshold_kernel(const float* __restrict__
   long long jj = (long long)ceilf(beta * (float)k * (float)m / (float)n);
   jj = jj < 1 ? 1 : (jj > m ? m : jj);
   const float* row = s + (int64_t)t * ld;
-  float x[EPT];
+  uint32_t key[EPT];
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int e = r * NT + tid;
-    x[r] = row[(int64_t)(e < m ? e : 0) * elem_step];
+    key[r] = __float_as_uint(row[(int64_t)(e < m ? e : 0) * elem_step]);
   }
-  uint32_t key[EPT];
   uint32_t mn = 0xffffffffu, mx = 0u;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const bool ok = r * NT + tid < m;
-    key[r] = ok ? float_key(x[r]) : 0u;
+    key[r] = ok ? float_key(__uint_as_float(key[r])) : 0u;
     if (ok) {
       mn = min(mn, key[r]);
       mx = max(mx, key[r]);
