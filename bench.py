@@ -7,8 +7,9 @@ One step = one indexer layer: all T = L query rows of a causal prefill scored
 against the L-key cache, top-k = 2048 per row (BASELINE.json configs[3] shape,
 the C4 workload of SURVEY.md §8).  Inputs are synthetic (torch randn keys and
 queries, softmax gates, seed 0) and device-resident for ``value``; ``e2e``
-repeats the step through the public estimator API with host->device copies of
-K/Q/W from pinned memory and a device->host read of the top-k each step.  The
+repeats the step through the public estimator API on pinned host K/Q/W: every
+step copies the inputs host->device and the top-k device->host, in row chunks
+whose copies overlap the scoring of the neighbouring chunks.  The
 queries (2 GiB) exceed the 126 MB L2, so no explicit L2 flush is used.
 
 Under torchrun (N > 1) the key axis is sharded block-cyclically across ranks,
@@ -296,10 +297,13 @@ def run_ours(a):
             est_engine = eng_m
 
         def step_e2e():
+            if world == 1:  # public API on pinned host tensors: copy-overlapped row-chunk pipeline
+                est.select_batch(Kh, Qh, Wh)
+                return
             Kd.copy_(Kh, non_blocking=True)
             Qd.copy_(Qh, non_blocking=True)
             Wd.copy_(Wh, non_blocking=True)
-            r = est.select_batch(Kd, Qd, Wd) if world == 1 else est_engine.run(Kd, Qd, Wd)
+            r = est_engine.run(Kd, Qd, Wd)
             out_h.copy_(r.topk, non_blocking=True)
 
         e2e_ms = max_over_ranks(_time_steps(step_e2e, a.steps, max(1, a.warmup), barrier))

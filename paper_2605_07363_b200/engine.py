@@ -489,6 +489,79 @@ class IndexerEngine:
         return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H],
                              candidates=tgt)
 
+    # ----------------------------------------------------------- host pipeline
+    def run_host(self, keys, queries, weights, prefix_len=None, *, chunks: int = 8,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+        """Host (ideally pinned) inputs -> host (T, k) top-k, with the copies overlapped.
+
+        Rows are split into ``chunks`` groups of about equal causal work; chunk c+1's
+        queries / gates are copied host->device on one stream while chunk c is scored on
+        the compute stream, and chunk c's result goes device->host on a third stream.  The
+        keys (small: L x d bf16) are uploaded once up front."""
+        Kh = torch.as_tensor(keys)
+        Qh = torch.as_tensor(queries)
+        Wh = torch.as_tensor(weights)
+        L, T = int(Kh.shape[0]), int(Qh.shape[0])
+        if prefix_len is None:
+            if T > L:
+                raise ValueError(f"causal prefill needs T <= L, got T={T}, L={L}")
+            pl = np.arange(L - T + 1, L + 1, dtype=np.int64)
+        else:
+            pl = np.asarray(prefix_len.cpu() if isinstance(prefix_len, torch.Tensor) else prefix_len,
+                            dtype=np.int64).reshape(-1)
+        dev = torch.device("cuda")
+        k = self.k
+        if out is None:
+            out = self._ws.get("host_out")
+            if out is None or tuple(out.shape) != (T, k):
+                out = torch.empty(T, k, dtype=torch.int32).pin_memory()
+                self._ws["host_out"] = out
+        # chunk boundaries with ~equal work (sum of prefix lengths)
+        cw = np.cumsum(pl)
+        cuts = [0] + [int(np.searchsorted(cw, cw[-1] * (c + 1) / chunks)) + 1 for c in range(chunks - 1)] + [T]
+        cuts = sorted(set(min(max(c, 0), T) for c in cuts))
+        spans = [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
+        rmax = max(b - a for a, b in spans)
+        comp = torch.cuda.current_stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        Kd = torch.empty(Kh.shape, dtype=Kh.dtype, device=dev)
+        Qd = [torch.empty((rmax,) + tuple(Qh.shape[1:]), dtype=Qh.dtype, device=dev) for _ in range(2)]
+        Wd = [torch.empty((rmax,) + tuple(Wh.shape[1:]), dtype=Wh.dtype, device=dev) for _ in range(2)]
+        Od = [torch.empty((rmax, k), dtype=torch.int32, device=dev) for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in spans]
+        ev_comp = [torch.cuda.Event() for _ in spans]
+        ev_out = [torch.cuda.Event() for _ in spans]
+
+        def upload(c):
+            a, b = spans[c]
+            buf = c % 2
+            with torch.cuda.stream(s_in):
+                if c >= 2:
+                    s_in.wait_event(ev_comp[c - 2])  # buffer pair reused from chunk c-2
+                if c == 0:
+                    Kd.copy_(Kh, non_blocking=True)
+                Qd[buf][: b - a].copy_(Qh[a:b], non_blocking=True)
+                Wd[buf][: b - a].copy_(Wh[a:b], non_blocking=True)
+                ev_in[c].record(s_in)
+
+        upload(0)
+        for c, (a, b) in enumerate(spans):
+            buf = c % 2
+            if c + 1 < len(spans):
+                upload(c + 1)  # next chunk's copy overlaps this chunk's scoring
+            comp.wait_event(ev_in[c])
+            if c >= 2:
+                comp.wait_event(ev_out[c - 2])  # result buffer drained
+            self.run(Kd, Qd[buf][: b - a], Wd[buf][: b - a], prefix_len=pl[a:b], out=Od[buf][: b - a])
+            ev_comp[c].record(comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_comp[c])
+                out[a:b].copy_(Od[buf][: b - a], non_blocking=True)
+                ev_out[c].record(s_out)
+        for e in ev_out:
+            comp.wait_event(e)
+        return out
+
     # ----------------------------------------------------------- entry
     def run(self, keys, queries, weights, prefix_len=None, *, need_importance: bool = False,
             out: torch.Tensor | None = None) -> IndexerOutput:

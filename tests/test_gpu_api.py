@@ -113,3 +113,20 @@ def test_errors_follow_reference_convention():
     with pytest.raises(ValueError):
         make_indexer("dense")
     assert len(MISAIndexer(budget_k=8, active_heads_h=32, block_size=8).select(w).heads) == 8
+
+
+def test_select_batch_host_pipeline_equals_device_path():
+    """Pinned host inputs take the copy-overlapped row-chunk pipeline; same top-k as on device."""
+    import torch
+    from paper_2605_07363_b200 import MISAIndexer
+    g = torch.Generator().manual_seed(4)
+    L, H, d = 12000, 64, 128
+    K = torch.randn(L, d, generator=g).bfloat16()
+    Q = torch.randn(L, H, d, generator=g).bfloat16()
+    W = torch.softmax(torch.randn(L, H, generator=g), -1).float()
+    est = MISAIndexer(budget_k=512, active_heads_h=8, block_size=1024)
+    host = est.select_batch(K.pin_memory(), Q.pin_memory(), W.pin_memory()).topk
+    torch.cuda.synchronize()
+    dev = est.select_batch(K.cuda(), Q.cuda(), W.cuda()).topk
+    torch.cuda.synchronize()
+    assert not host.is_cuda and torch.equal(host, dev.cpu())
