@@ -315,16 +315,16 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int x) {
 // value and costs one atomic per sample and three barriers per row.  The kernel is
 // kept lean (registers, 9 KB smem) so that many rows are in flight per SM.
 template <int NT, int EPT>
-__global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kernel(const float* __restrict__ s, int64_t ld,
-                                                       const int32_t* __restrict__ prefix_len, int stride, int k,
-                                                       float beta, int64_t append_all, float* __restrict__ tau,
-                                                       int elem_step = 1) {
+__device__ __forceinline__ void threshold_row(int t, const float* __restrict__ s, int64_t ld,
+                                              const int32_t* __restrict__ prefix_len, int stride, int k,
+                                              float beta, int64_t append_all, float* __restrict__ tau,
+                                              int elem_step) {
   constexpr int NW = NT / 32, NB = 2048, BPT = NB / NT;
   __shared__ uint32_t hist[NB];
   __shared__ uint32_t rmin[NW], rmax[NW];
   __shared__ int wsum[NW];
   __shared__ int sh_bin, sh_above, sh_above_new;
-  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int n = prefix_len[t];
   if (n <= append_all || n <= k) {
     if (tid == 0) tau[t] = -INFINITY;
@@ -364,12 +364,17 @@ __global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kern
     mn = min(mn, rmin[i]);
     mx = max(mx, rmax[i]);
   }
-  uint32_t lo = mn;
-  uint32_t span = mx - mn;  // window [lo, lo + span]
+  // First try a window of the top 2^23 key ulps below the maximum (one binary order of
+  // magnitude, [max/2, max] for positive scores — where the j-th largest of a 1/32 sample,
+  // the top few %, normally lies): 2048 bins of 2^12 ulps = 2^-11 relative, one level.  If
+  // the j-th sample is below that window, bin the whole range [min, max] and refine the
+  // boundary bin once.
+  bool narrow = mx - mn > (1u << 23);
+  uint32_t lo = narrow ? mx - (1u << 23) : mn;
+  uint32_t span = mx - lo;  // window [lo, lo + span]
   int sft = span == 0u ? 0 : max(0, 32 - __clz(span) - 11);
-  // level 1 bins the whole sampled range; a coarse boundary bin (wider than 2^12 key ulps,
-  // i.e. ~2^-11 relative) is re-binned once at 2^-11 of its width
   for (int level = 0;; ++level) {
+    if (tid == 0) sh_bin = -1;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
       const uint32_t d = key[r] - lo;
@@ -392,8 +397,7 @@ __global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kern
     }
     if (lane == 31) wsum[w] = incl;
     __syncthreads();
-    int above = incl - tot + (level ? sh_above : 0);
-    for (int i = 0; i < w; ++i) above += wsum[i];
+    int above = incl - tot + (level ? sh_above : 0) + warps_exclusive<NW>(wsum, w);
     if (above < jj && jj <= above + tot) {
 #pragma unroll
       for (int i = 0; i < BPT; ++i) {
@@ -407,9 +411,18 @@ __global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kern
 #pragma unroll
     for (int i = 0; i < BPT; ++i) hist[tid * BPT + i] = 0u;
     __syncthreads();
-    const uint32_t b = (uint32_t)sh_bin;
-    lo += b << sft;
-    if (level == 1 || sft <= 12) {
+    const int bin = sh_bin;
+    if (bin < 0) {  // the j-th sample lies below the narrow window: whole range, two levels
+      narrow = false;
+      lo = mn;
+      span = mx - mn;
+      sft = span == 0u ? 0 : max(0, 32 - __clz(span) - 11);
+      level = -1;
+      __syncthreads();
+      continue;
+    }
+    lo += (uint32_t)bin << sft;
+    if (narrow || level == 1 || sft <= 12) {
       if (tid == 0) tau[t] = key_float(lo);  // lower edge of the bin: <= the j-th sample
       return;
     }
@@ -417,6 +430,17 @@ __global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kern
     sft = sft - 11;
     if (tid == 0) sh_above = sh_above_new;  // samples above the refined window
     __syncthreads();
+  }
+}
+
+// Persistent over rows (a CTA per row would pay a block launch per ~3K-cycle row).
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kernel(
+    const float* __restrict__ s, int64_t ld, const int32_t* __restrict__ prefix_len, int n_rows, int stride, int k,
+    float beta, int64_t append_all, float* __restrict__ tau, int elem_step = 1) {
+  for (int t = blockIdx.x; t < n_rows; t += gridDim.x) {
+    threshold_row<NT, EPT>(t, s, ld, prefix_len, stride, k, beta, append_all, tau, elem_step);
+    __syncthreads();  // histogram / scan scratch reused by the next row
   }
 }
 
@@ -1654,11 +1678,19 @@ int dispatch_capacity(int64_t n, cudaStream_t st, Args... args) {
   return -100;  // caller falls back
 }
 
+template <typename K>
+static unsigned persistent_grid(K kern, int nt, int64_t rows) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  return (unsigned)std::min<int64_t>(rows, (int64_t)sm_count() * per_sm);
+}
+
 template <int NT, int EPT>
 struct ThresholdL {
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
                 float beta, int64_t aa, float* tau) {
-    threshold_kernel<NT, EPT><<<(unsigned)T, NT, 0, st>>>(s, ld, pl, stride, k, beta, aa, tau);
+    threshold_kernel<NT, EPT><<<persistent_grid(threshold_kernel<NT, EPT>, NT, T), NT, 0, st>>>(
+        s, ld, pl, (int)T, stride, k, beta, aa, tau);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
   }
@@ -1668,7 +1700,8 @@ template <int NT, int EPT>
 struct ThresholdStepL {  // samples every `stride`-th element of a dense row
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
                 float beta, int64_t aa, float* tau) {
-    threshold_kernel<NT, EPT><<<(unsigned)T, NT, 0, st>>>(s, ld, pl, stride, k, beta, aa, tau, stride);
+    threshold_kernel<NT, EPT><<<persistent_grid(threshold_kernel<NT, EPT>, NT, T), NT, 0, st>>>(
+        s, ld, pl, (int)T, stride, k, beta, aa, tau, stride);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
   }
