@@ -122,8 +122,9 @@ __global__ void __launch_bounds__(kRefThreads, 1)
 
   if (warp < kRefProd) {
     // ---------------------------------------------------------------- producers
-    // warp p covers tile rows [32p, 32p + 32): instruction i moves rows 32p + 2i and
-    // 32p + 2i + 1 (lanes 0-15 / 16-31, one 16-byte chunk each)
+    // warp p covers tile rows [RPW p, RPW p + RPW): instruction i moves rows RPW p + 2i and
+    // RPW p + 2i + 1 (lanes 0-15 / 16-31, one 16-byte chunk each)
+    constexpr int RPW = 128 / kRefProd;
     const int p = warp, half = lane >> 4, ch = lane & 15;
     int s = 0;
     uint32_t ph = 0;
@@ -148,20 +149,20 @@ __global__ void __launch_bounds__(kRefThreads, 1)
         }
       }
       const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
-      // lane holds the index of tile row 32p + lane, kIdxAhead tiles ahead (register ring)
+      // lane (< RPW) holds the index of tile row RPW p + lane, kIdxAhead tiles ahead
       constexpr int kIdxAhead = 4;
       int ring[kIdxAhead];
 #pragma unroll
       for (int d = 0; d < kIdxAhead; ++d) {
-        const int i = d * 128 + 32 * p + lane;
-        ring[d] = (d < nt && i < nc) ? __ldg(cr + i) : -1;
+        const int i = d * 128 + RPW * p + lane;
+        ring[d] = (d < nt && lane < RPW && i < nc) ? __ldg(cr + i) : -1;
       }
       for (int j = 0; j < nt; ++j) {
         ptx::mbar_wait(&empty_a[s], ph ^ 1);
         uint8_t* stage = sA + s * C::A_BYTES;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int r = 32 * p + 2 * i + half;
+        for (int i = 0; i < RPW / 2; ++i) {
+          const int r = RPW * p + 2 * i + half;
           const int ki = __shfl_sync(0xffffffffu, ring[0], 2 * i + half);
           const __nv_bfloat16* src = a.keys + (int64_t)(ki < 0 ? 0 : ki) * D + ch * 8;
           if (ch * 8 < D)
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(kRefThreads, 1)
         cp_async_mbar_arrive(&full_a[s]);
 #pragma unroll
         for (int d = 0; d + 1 < kIdxAhead; ++d) ring[d] = ring[d + 1];
-        const int i = (j + kIdxAhead) * 128 + 32 * p + lane;
-        ring[kIdxAhead - 1] = (j + kIdxAhead < nt && i < nc) ? __ldg(cr + i) : -1;
+        const int i = (j + kIdxAhead) * 128 + RPW * p + lane;
+        ring[kIdxAhead - 1] = (j + kIdxAhead < nt && lane < RPW && i < nc) ? __ldg(cr + i) : -1;
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }

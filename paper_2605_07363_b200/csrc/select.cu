@@ -364,13 +364,13 @@ __device__ __forceinline__ void threshold_row(int t, const float* __restrict__ s
     mn = min(mn, rmin[i]);
     mx = max(mx, rmax[i]);
   }
-  // First try a window of the top 2^23 key ulps below the maximum (one binary order of
-  // magnitude, [max/2, max] for positive scores — where the j-th largest of a 1/32 sample,
-  // the top few %, normally lies): 2048 bins of 2^12 ulps = 2^-11 relative, one level.  If
+  // First try a window of the top 2^24 key ulps below the maximum (two binary orders of
+  // magnitude, [max/4, max] for positive scores — where the j-th largest of a 1/32 sample,
+  // the top few %, normally lies): 2048 bins of 2^13 ulps = 2^-10 relative, one level.  If
   // the j-th sample is below that window, bin the whole range [min, max] and refine the
   // boundary bin once.
-  bool narrow = mx - mn > (1u << 23);
-  uint32_t lo = narrow ? mx - (1u << 23) : mn;
+  bool narrow = mx - mn > (1u << 24);
+  uint32_t lo = narrow ? mx - (1u << 24) : mn;
   uint32_t span = mx - lo;  // window [lo, lo + span]
   int sft = span == 0u ? 0 : max(0, 32 - __clz(span) - 11);
   for (int level = 0;; ++level) {
@@ -435,7 +435,7 @@ __device__ __forceinline__ void threshold_row(int t, const float* __restrict__ s
 
 // Persistent over rows (a CTA per row would pay a block launch per ~3K-cycle row).
 template <int NT, int EPT>
-__global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 2)) threshold_kernel(
+__global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 1)) threshold_kernel(
     const float* __restrict__ s, int64_t ld, const int32_t* __restrict__ prefix_len, int n_rows, int stride, int k,
     float beta, int64_t append_all, float* __restrict__ tau, int elem_step = 1) {
   for (int t = blockIdx.x; t < n_rows; t += gridDim.x) {
@@ -1679,7 +1679,8 @@ int dispatch_capacity(int64_t n, cudaStream_t st, Args... args) {
 }
 
 template <typename K>
-static unsigned persistent_grid(K kern, int nt, int64_t rows) {
+static unsigned persistent_grid(K kern, int nt, int64_t rows, bool persistent = true) {
+  if (!persistent) return (unsigned)rows;  // one CTA per row
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
   return (unsigned)std::min<int64_t>(rows, (int64_t)sm_count() * per_sm);
@@ -1689,7 +1690,7 @@ template <int NT, int EPT>
 struct ThresholdL {
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
                 float beta, int64_t aa, float* tau) {
-    threshold_kernel<NT, EPT><<<persistent_grid(threshold_kernel<NT, EPT>, NT, T), NT, 0, st>>>(
+    threshold_kernel<NT, EPT><<<persistent_grid(threshold_kernel<NT, EPT>, NT, T, NT * EPT <= 4096), NT, 0, st>>>(
         s, ld, pl, (int)T, stride, k, beta, aa, tau);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
@@ -1700,7 +1701,7 @@ template <int NT, int EPT>
 struct ThresholdStepL {  // samples every `stride`-th element of a dense row
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
                 float beta, int64_t aa, float* tau) {
-    threshold_kernel<NT, EPT><<<persistent_grid(threshold_kernel<NT, EPT>, NT, T), NT, 0, st>>>(
+    threshold_kernel<NT, EPT><<<persistent_grid(threshold_kernel<NT, EPT>, NT, T, NT * EPT <= 4096), NT, 0, st>>>(
         s, ld, pl, (int)T, stride, k, beta, aa, tau, stride);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
