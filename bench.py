@@ -59,6 +59,7 @@ def _args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--hier", action="store_true", help="also time MISA-dagger (k'=--kprime)")
     p.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
+    p.add_argument("--no-sweep", action="store_true", help="skip the C2 / C3 prefill configs")
     return p.parse_args()
 
 
@@ -271,6 +272,27 @@ def run_ours(a):
     else:
         res_d = _Out(eng_d.run(K, Q, W, gather=True))
 
+    # --- the other BASELINE.json prefill configs (C2 DSv3.2 32K, C3 GLM-5 H=32 64K), 1 GPU
+    sweep = None
+    if world == 1 and not a.no_sweep:
+        sweep = []
+        for name, Ls, Hs in (("C2 DeepSeek-V3.2 shape, causal prefill L=T=32768, H=64, h=8", 32768, 64),
+                             ("C3 GLM-5 shape, causal prefill L=T=65536, H=32, h=8", 65536, 32)):
+            g3 = torch.Generator(device="cuda").manual_seed(2)
+            Ks = torch.randn(Ls, a.d, device="cuda", generator=g3).bfloat16()
+            Qs = torch.randn(Ls, Hs, a.d, device="cuda", generator=g3).bfloat16()
+            Ws = torch.softmax(torch.randn(Ls, Hs, device="cuda", generator=g3), -1).float()
+            xs = prepare_inputs(Ks, Qs, Ws)
+            em = IndexerEngine("misa", budget_k=a.k, active_heads_h=a.h, block_size=a.B)
+            ed = IndexerEngine("dsa", budget_k=a.k)
+            ms_m = _time_steps(lambda: em.run_prepared(xs), 10, 3, barrier)
+            ms_d = _time_steps(lambda: ed.run_prepared(xs), 5, 2, barrier)
+            Ps = Ls * (Ls + 1) // 2
+            sweep.append({"workload": name, "misa_ms": round(ms_m, 3), "dsa_ms": round(ms_d, 3),
+                          "speedup_vs_dsa": round(ms_d / ms_m, 3), "misa_scores_per_s": Ps / (ms_m * 1e-3),
+                          "misa_tensor_frac": round(2.0 * a.h * a.d * Ps / (ms_m * 1e-3) / 1e12 / tc_sust, 4)})
+            del Ks, Qs, Ws, xs, em, ed
+
     hier_ms = None
     hstages = {}
     if a.hier and world == 1:
@@ -410,7 +432,7 @@ def run_ours(a):
         "dsa_stages_ms": {k: round(v, 4) for k, v in dstages.items()},
         "fallback_rows": fallback,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
-        "decode": decode, "sharded_decode": sdec,
+        "decode": decode, "sharded_decode": sdec, "configs": sweep,
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)
