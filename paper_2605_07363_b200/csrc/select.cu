@@ -662,6 +662,12 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
     if (cB <= kBucketMax || sft == 0) break;
     sft = max(0, sft - 11);
   }
+  // the whole boundary bin is selected: the cut is its lower edge (no collect / rank)
+  if (need == cB) {
+    v_out = lo == 0u ? 0u : lo - 1u;  // selected iff key > lo - 1, i.e. key >= lo
+    thr_out = -1;
+    return;
+  }
   // elements of the boundary bin: keys in [lo, lo + span_m1]
   if (cB <= kBucketMax) {
 #pragma unroll
@@ -693,9 +699,8 @@ __device__ void hist_cut(const uint32_t (&key)[EPT], IdxFn idx_of, int N, int kk
     __syncthreads();
     CUT_MARK(13);
     if (threadIdx.x == 0 && blockIdx.x == 0) CUT_MARK_CB(cB);
-    v_out = sh.res_v;
+    v_out = sh.res_v;  // res_* are next written by a later row's rank phase, many barriers on
     thr_out = sh.res_thr;
-    __syncthreads();
     return;
   }
   // more than kBucketMax copies of one key value: keep the `need` smallest indices
