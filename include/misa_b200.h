@@ -23,6 +23,7 @@
  *   misa_route_select     routing.py:38-75   route_head_importance epilogue + route_topk_heads
  *   misa_score_materialize dsa.py:37-61, routing.py:78-99  gated_relu_scores / dsa_score / misa_score
  *   misa_score_materialize_split  the same, key-axis split (decode)
+ *   misa_score_materialize_paged  the same over a paged key cache (decode)
  *   misa_score_filter     dsa.py:37-76 fused with the candidate pass of topk_tokens
  *   misa_select_threshold (no reference counterpart: sampled threshold for the fused top-k)
  *   misa_select_topk      dsa.py:64-76       topk_tokens over the filtered candidates
@@ -110,6 +111,15 @@ int misa_score_materialize_split(const void* keys, int64_t n_keys, int64_t key_s
                                  const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
                                  int64_t n_rows, const int32_t* items, const int32_t* item_tiles,
                                  const int32_t* item_tile0, int n_items, float* out, int64_t out_ld, void* stream);
+
+/* materialize over a paged key cache (decode): logical key s of every row lives at pool row
+ * page_table[s / page_size] * page_size + s % page_size (page_size a multiple of 128). */
+int misa_score_materialize_paged(const void* key_pool, int64_t n_pool_keys, int head_dim, const void* queries,
+                                 const float* weights, int n_heads, int n_heads_pad, const int32_t* heads,
+                                 int heads_per_query, const int32_t* prefix_len, int64_t n_rows,
+                                 const int32_t* items, const int32_t* item_tiles, const int32_t* item_tile0,
+                                 int n_items, const int32_t* page_table, int page_size, float* out, int64_t out_ld,
+                                 void* stream);
 
 /* filter: append (score, s) with score >= tau[t] to cand[(t*4 + w)*cap + i] (w = TMEM lane
  * quadrant of the key within its tile); cand_count[t*4 + w] = total seen (may exceed cap). */

@@ -17,7 +17,7 @@ from .workload import (IndexerWorkload, NeedleLabel, gen_needle_workload, gen_ra
                        save_workload, softmax)
 from .metrics import candidate_recall, cost_ratio, iou, needle_recall
 from .engine import DecodeGraph, IndexerEngine, IndexerOutput, prepare_inputs
-from .pooling import BlockSummary, PooledKeyCache, build_block_summary, incremental_append
+from .pooling import BlockSummary, PagedKeyCache, PooledKeyCache, build_block_summary, incremental_append
 from .dsa import dsa_rescore, dsa_score, dsa_select, gated_relu_scores, relevance_dots, topk_tokens, topk_within
 from .routing import misa_hier_select, misa_score, misa_select, route_head_importance, route_topk_heads
 from .estimators import (INDEXER_REGISTRY, METHODS, BaseTokenIndexer, DSAIndexer, HierarchicalMISAIndexer,
@@ -26,7 +26,7 @@ from .estimators import (INDEXER_REGISTRY, METHODS, BaseTokenIndexer, DSAIndexer
 __version__ = "0.1.0"
 
 __all__ = [
-    "DecodeGraph",
+    "DecodeGraph", "PagedKeyCache",
     "BASELINE_BLOCK_SIZE", "BLOCK_ATTENTION", "BaseTokenIndexer", "BlockSummary", "CostEntry", "CostLedger",
     "DSAIndexer", "FAST32", "GATE_ONLY", "HeadSet", "HierarchicalMISAIndexer", "INDEXER_REGISTRY", "IndexerConfig",
     "IndexerEngine", "IndexerOutput", "IndexerWorkload", "METHODS", "MISAIndexer", "NeedleLabel", "PRECISION_MODES",

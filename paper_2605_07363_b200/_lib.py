@@ -36,6 +36,8 @@ SIGNATURES: dict[str, list] = {
                                _vp, _i64, _vp],
     "misa_score_materialize_split": [_vp, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, _vp,
                                      _vp, _i32, _vp, _i64, _vp],
+    "misa_score_materialize_paged": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp,
+                                     _i32, _vp, _i32, _vp, _i64, _vp],
     "misa_score_filter": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _i32, _vp, _vp,
                           _i32, _vp, _vp],
     "misa_select_threshold": [_vp, _i64, _vp, _i64, _i32, _i32, _f32, _i64, _vp, _vp],

@@ -132,6 +132,8 @@ struct ScoreArgs {
   const int32_t* __restrict__ items;
   const int32_t* __restrict__ item_tiles;
   const int32_t* __restrict__ item_tile0;  // MATERIALIZE key split: first tile of item i (null: 0)
+  const int32_t* __restrict__ page_table;  // paged key cache: logical page -> physical page (null: flat)
+  int page_tiles;                          // 128-key tiles per page
   int n_items;
   int T, H, Hp;
   int key_stride;
@@ -234,10 +236,13 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         for (int j = 0; j < nt; ++j) {
           ptx::mbar_wait(&empty_a[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
+          const int jj = j0 + j;  // logical tile -> row of the (possibly paged) key pool
+          const int row = a.page_table ? a.page_table[jj / a.page_tiles] * (a.page_tiles * kTileKeys) +
+                                             (jj % a.page_tiles) * kTileKeys
+                                       : jj * kTileKeys;
 #pragma unroll
           for (int at = 0; at < D / 64; ++at)
-            ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_k, &full_a[s], at * 64,
-                             (j0 + j) * kTileKeys);
+            ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_k, &full_a[s], at * 64, row);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -577,6 +582,43 @@ extern "C" int misa_score_materialize_split(const void* keys, int64_t n_keys, in
   a.H = n_heads;
   a.Hp = n_heads_pad;
   a.key_stride = static_cast<int>(key_stride);
+  a.out = out;
+  a.out_ld = out_ld;
+  return dispatch_score<false>(head_dim, heads_per_query, map, a, as_stream(stream));
+}
+
+extern "C" int misa_score_materialize_paged(const void* key_pool, int64_t n_pool_keys, int head_dim,
+                                            const void* queries, const float* weights, int n_heads, int n_heads_pad,
+                                            const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
+                                            int64_t n_rows, const int32_t* items, const int32_t* item_tiles,
+                                            const int32_t* item_tile0, int n_items, const int32_t* page_table,
+                                            int page_size, float* out, int64_t out_ld, void* stream) {
+  int rc = check_common(n_pool_keys, head_dim, n_heads, n_heads_pad, heads_per_query, n_rows, key_pool, queries,
+                        weights, prefix_len, items, item_tiles, n_items);
+  if (rc) return rc;
+  MISA_REQUIRE(out && out_ld >= 1 && page_table, "null output / page table");
+  MISA_REQUIRE(page_size >= kTileKeys && page_size % kTileKeys == 0, "page_size must be a multiple of %d",
+               kTileKeys);
+  MISA_REQUIRE(n_pool_keys % page_size == 0, "the key pool must hold whole pages");
+  MISA_REQUIRE(heads != nullptr || heads_per_query >= n_heads, "dense scoring needs heads_per_query >= n_heads");
+  CUtensorMap map;
+  rc = make_tmap_bf16_2d(&map, key_pool, head_dim, n_pool_keys, head_dim, kTileKeys);
+  if (rc) return rc;
+  ScoreArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.w = weights;
+  a.heads = heads;
+  a.prefix_len = prefix_len;
+  a.items = items;
+  a.item_tiles = item_tiles;
+  a.item_tile0 = item_tile0;
+  a.page_table = page_table;
+  a.page_tiles = page_size / kTileKeys;
+  a.n_items = n_items;
+  a.T = static_cast<int>(n_rows);
+  a.H = n_heads;
+  a.Hp = n_heads_pad;
+  a.key_stride = 1;
   a.out = out;
   a.out_ld = out_ld;
   return dispatch_score<false>(head_dim, heads_per_query, map, a, as_stream(stream));

@@ -90,6 +90,7 @@ class PreparedInputs:
     d: int
     D: int
     causal_key: tuple | None
+    pages: tuple | None = None  # paged key cache: (page_table (n_pages,) int32 device, page_size)
 
 
 def prepare_inputs(keys, queries, weights, prefix_len=None, device=None) -> PreparedInputs:
@@ -137,6 +138,35 @@ def prepare_inputs(keys, queries, weights, prefix_len=None, device=None) -> Prep
             raise ValueError("prefix lengths must lie in [1, L]")
     prefix = torch.from_numpy(host.astype(np.int32)).to(dev)
     return PreparedInputs(K, Q, W, prefix, host, L, T, H, Hp, d, D, causal_key)
+
+
+def paged_inputs(cache, queries, weights, prefix_len=None) -> PreparedInputs:
+    """Decode inputs over a ``PagedKeyCache``: keys stay in the page pool (the scorer
+    translates logical tiles through the page table); every row sees the whole cache."""
+    dev = cache.pool_keys.device
+    Q = torch.as_tensor(queries, device=dev)
+    W = torch.as_tensor(weights, device=dev)
+    if Q.ndim != 3 or W.ndim != 2 or tuple(W.shape) != tuple(Q.shape[:2]):
+        raise ValueError("queries must be (T, H, d) and weights (T, H)")
+    T, H, d = Q.shape
+    if d != cache.d:
+        raise ValueError(f"queries have dim {d}, the cache holds dim {cache.d}")
+    D, Hp, L = cache.D, heads_pad(H), cache.length
+    if L < 1:
+        raise ValueError("empty cache")
+    Q = Q.to(torch.bfloat16)
+    if d != D or H != Hp:
+        Q = torch.nn.functional.pad(Q, (0, D - d, 0, Hp - H))
+    W = W.to(torch.float32)
+    if H != Hp:
+        W = torch.nn.functional.pad(W, (0, Hp - H))
+    host = np.full(T, L, dtype=np.int64) if prefix_len is None else np.asarray(
+        prefix_len.cpu() if isinstance(prefix_len, torch.Tensor) else prefix_len, dtype=np.int64).reshape(-1)
+    if host.shape[0] != T or np.any(host != L):
+        raise ValueError("paged decode scores every row against the whole cache (prefix_len == cache.length)")
+    prefix = torch.from_numpy(host.astype(np.int32)).to(dev)
+    return PreparedInputs(cache.pool_keys, Q.contiguous(), W.contiguous(), prefix, host, L, T, H, Hp, d, D,
+                          ("paged", L, T), pages=(cache.page_table, cache.B))
 
 
 class IndexerEngine:
@@ -278,7 +308,9 @@ class IndexerEngine:
             if cache is not None:
                 if cache.B != self.B:
                     raise ValueError(f"cache block size {cache.B} != engine block_size {self.B}")
-                P, planes, rows = cache.prefix, cache.planes, cache.rows
+                # a paged cache hands out the address that maps its shared partial block
+                P = cache.prefix_base(x.L) if getattr(cache, "paged", False) else cache.prefix
+                planes, rows = cache.planes, cache.rows
                 n_chunks = max(1, (x.L // self.B + 127) // 128)
             else:
                 P, planes, n_chunks, rows = self.pool(x)
@@ -287,7 +319,8 @@ class IndexerEngine:
                                                         dev)
             partial = self._buf("partial", (n_chunks, x.T, x.Hp), torch.float32, dev)
             self._mark("route_scores")
-            _lib.call("misa_route_scores", _ptr(x.queries), x.T, x.Hp, x.D, _ptr(planes), rows, _ptr(P),
+            _lib.call("misa_route_scores", _ptr(x.queries), x.T, x.Hp, x.D, _ptr(planes), rows,
+                      P if isinstance(P, int) else _ptr(P),
                       _ptr(x.prefix), self.B, _ptr(it_tile), _ptr(it_chunk), _ptr(it_cols), it_tile.numel(),
                       _ptr(partial), self._stream())
         self._mark("route_select")
@@ -415,9 +448,15 @@ class IndexerEngine:
                                              lambda: self.split_items(x.prefix_host, G, target), dev)
         rows = self._buf("dense_rows", (x.T, x.L), torch.float32, dev)
         self._mark("decode:score")
-        _lib.call("misa_score_materialize_split", _ptr(x.keys), x.L, 1, x.D, _ptr(x.queries), _ptr(x.weights), x.H,
-                  x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles), _ptr(tile0), items.numel(),
-                  _ptr(rows), x.L, self._stream())
+        if x.pages is not None:
+            table, page = x.pages
+            _lib.call("misa_score_materialize_paged", _ptr(x.keys), x.keys.shape[0], x.D, _ptr(x.queries),
+                      _ptr(x.weights), x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles),
+                      _ptr(tile0), items.numel(), _ptr(table), page, _ptr(rows), x.L, self._stream())
+        else:
+            _lib.call("misa_score_materialize_split", _ptr(x.keys), x.L, 1, x.D, _ptr(x.queries), _ptr(x.weights),
+                      x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles), _ptr(tile0),
+                      items.numel(), _ptr(rows), x.L, self._stream())
         return rows
 
     def dense_select(self, x: PreparedInputs, heads, hq: int, k: int, out: torch.Tensor,
@@ -453,6 +492,11 @@ class IndexerEngine:
         and the router's pooled state come from the incrementally maintained cache.
         Row t equals the reference on ``IndexerWorkload(K[:n_t], Q[t], W[t])``; the
         default prefix is the whole cache / key set for every row."""
+        if cache is not None and getattr(cache, "paged", False):
+            if self.method == "misa_hier":
+                raise ValueError("misa_hier decode needs a contiguous key cache (PooledKeyCache)")
+            x = paged_inputs(cache, queries, weights, prefix_len)
+            return self.decode_prepared(x, cache=cache, need_importance=need_importance, out=out)
         if cache is not None:
             keys = cache.keys[:cache.length, :cache.d]
         if keys is None or queries is None or weights is None:
@@ -607,7 +651,12 @@ class DecodeGraph:
     def __init__(self, engine: "IndexerEngine", cache, n_rows: int, n_heads: int, bucket: int = 4096):
         self.engine, self.cache, self.T, self.H = engine, cache, int(n_rows), int(n_heads)
         self.bucket = check_positive_int(bucket, "bucket")
-        dev = cache.keys.device
+        self.paged = bool(getattr(cache, "paged", False))
+        if self.paged:
+            if engine.method == "misa_hier":
+                raise ValueError("misa_hier decode needs a contiguous key cache (PooledKeyCache)")
+            self.bucket = cache.B  # the router's partial-block address is fixed within one page
+        dev = (cache.pool_keys if self.paged else cache.keys).device
         self.Hp = heads_pad(self.H)
         self.q = torch.zeros(self.T, self.Hp, cache.D, dtype=torch.bfloat16, device=dev)
         self.w = torch.zeros(self.T, self.Hp, dtype=torch.float32, device=dev)
@@ -619,8 +668,13 @@ class DecodeGraph:
 
     def _capture(self, Lb: int) -> None:
         c = self.cache
-        x = PreparedInputs(c.keys[:Lb], self.q, self.w, self.prefix, np.full(self.T, Lb, dtype=np.int64), Lb,
-                           self.T, self.H, self.Hp, c.d, c.D, ("decode", Lb, self.T))
+        host = np.full(self.T, Lb, dtype=np.int64)
+        if self.paged:
+            x = PreparedInputs(c.pool_keys, self.q, self.w, self.prefix, host, Lb, self.T, self.H, self.Hp, c.d, c.D,
+                               ("decode-paged", Lb, self.T), pages=(c.page_table, c.B))
+        else:
+            x = PreparedInputs(c.keys[:Lb], self.q, self.w, self.prefix, host, Lb, self.T, self.H, self.Hp, c.d,
+                               c.D, ("decode", Lb, self.T))
         eng = self.engine
         self.prefix.fill_(max(1, min(c.length, Lb)))  # warm-up on a valid prefix
         stream = torch.cuda.Stream()

@@ -146,8 +146,12 @@ class PooledKeyCache:
         if self.length + n > self.capacity:
             raise ValueError("PooledKeyCache capacity exceeded")
         self.keys[self.length:self.length + n, :self.d] = kr.to(torch.bfloat16)
-        for i in range(n):
-            _lib.call("misa_pool_append", self.keys.data_ptr(), self.length + i, self.D, self.B,
+        if n <= 8:  # decode: one append launch per key (pooling.py:87-115)
+            for i in range(n):
+                _lib.call("misa_pool_append", self.keys.data_ptr(), self.length + i, self.D, self.B,
+                          self.prefix.data_ptr(), None, self.planes.data_ptr(), self.rows, _stream())
+        else:  # bulk (prefill): re-pool the whole prefix in one launch (O(L), ~0.2 ms at 1M keys)
+            _lib.call("misa_pool_keys", self.keys.data_ptr(), self.length + n, self.D, self.B,
                       self.prefix.data_ptr(), None, self.planes.data_ptr(), self.rows, _stream())
         self.length += n
 
@@ -158,3 +162,77 @@ class PooledKeyCache:
         rem = L - nf * B
         out = full if not rem else torch.cat([full, (self.prefix[L - 1, :d].double() / rem)[None]], 0)
         return BlockSummary(B, _bounds(L, B), out.cpu().numpy())
+
+
+class PagedKeyCache:
+    """Paged decode state: keys and in-block prefix sums live in fixed-size pages of one
+    pool (page = pooled block, a multiple of 128 keys), reached through a page table;
+    the pooled planes of the full blocks stay contiguous (one small row per block).
+
+    Pages are taken from a free list in any order (``page_order`` shuffles it to prove
+    the indirection), so a serving system can share the pool across sequences.  The
+    scorer translates logical 128-key tiles through the table
+    (``misa_score_materialize_paged``); the router needs only the pooled planes and the
+    partial block's running sum, whose address ``prefix_base`` hands out."""
+
+    paged = True
+
+    def __init__(self, head_dim: int, block_size: int, n_pages: int, device="cuda", page_order=None):
+        self.d = head_dim
+        self.D = head_dim_pad(head_dim)
+        self.B = check_positive_int(block_size, "block_size")
+        if self.B % 128:
+            raise ValueError("pages hold whole 128-key tiles: block_size must be a multiple of 128")
+        self.n_pages = check_positive_int(n_pages, "n_pages")
+        self.capacity = self.n_pages * self.B
+        self.pool_keys = torch.zeros(self.capacity, self.D, dtype=torch.bfloat16, device=device)
+        self.pool_prefix = torch.zeros(self.capacity, self.D, dtype=torch.float32, device=device)
+        self.rows = max(128, (self.n_pages + 127) // 128 * 128)
+        self.planes = torch.zeros(3, self.rows, self.D, dtype=torch.bfloat16, device=device)
+        self.page_table = torch.full((self.n_pages,), -1, dtype=torch.int32, device=device)
+        self._tmp_planes = torch.zeros(3, 1, self.D, dtype=torch.bfloat16, device=device)
+        self.free = list(range(self.n_pages)) if page_order is None else [int(p) for p in page_order]
+        if sorted(self.free) != list(range(self.n_pages)):
+            raise ValueError("page_order must be a permutation of the pool's pages")
+        self.pages: list[int] = []
+        self.length = 0
+
+    def _phys(self, i: int) -> int:
+        return self.pages[i // self.B] * self.B + i % self.B
+
+    def prefix_base(self, L: int) -> int:
+        """Address P such that P + (L-1)*D*4 is key L-1's in-block prefix sum (router)."""
+        return self.pool_prefix.data_ptr() + (self._phys(L - 1) - (L - 1)) * self.D * 4
+
+    def append(self, key_rows) -> None:
+        kr = torch.as_tensor(key_rows, device=self.pool_keys.device).reshape(-1, self.d).to(torch.bfloat16)
+        n = kr.shape[0]
+        if self.length + n > self.capacity:
+            raise ValueError("PagedKeyCache capacity exceeded")
+        D, B = self.D, self.B
+        pos = 0
+        while pos < n:
+            L = self.length
+            if L % B == 0:  # open a page
+                page = self.free.pop(0)
+                self.page_table[len(self.pages)] = page
+                self.pages.append(page)
+            page = self.pages[L // B]
+            off = L % B
+            m = min(n - pos, B - off)
+            base = page * B
+            self.pool_keys[base + off:base + off + m, :self.d] = kr[pos:pos + m]
+            if m <= 8:
+                for i in range(m):  # decode append into the page (logical index via an offset base)
+                    _lib.call("misa_pool_append", self.pool_keys.data_ptr() + (base - (L - off)) * D * 2, L + i, D, B,
+                              self.pool_prefix.data_ptr() + (base - (L - off)) * D * 4, None,
+                              self.planes.data_ptr(), self.rows, _stream())
+            else:  # re-pool the page's keys so far: one block, exactly the full-prefix pooling of it
+                full = off + m == B
+                _lib.call("misa_pool_keys", self.pool_keys.data_ptr() + base * D * 2, off + m, D, B,
+                          self.pool_prefix.data_ptr() + base * D * 4, None,
+                          self._tmp_planes.data_ptr() if full else None, 1, _stream())
+                if full:
+                    self.planes[:, L // B].copy_(self._tmp_planes[:, 0])
+            self.length += m
+            pos += m

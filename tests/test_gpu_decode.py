@@ -163,3 +163,53 @@ def test_virtual_key_shards_decode_merge_to_single_gpu(method, G):
     _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, T * k, T, k, k, out.data_ptr(), k, stream)
     torch.cuda.synchronize()
     assert torch.equal(out, ref.topk)
+
+
+@pytest.mark.parametrize("method", ["misa", "dsa"])
+def test_paged_key_cache_decode_equals_contiguous(method):
+    """Keys in shuffled pages of a PagedKeyCache (bulk and per-token appends, partial last
+    page) decode exactly like the contiguous cache: heads and top-k bit-identical."""
+    from paper_2605_07363_b200 import DecodeGraph, IndexerEngine, PagedKeyCache
+    from paper_2605_07363_b200.pooling import PooledKeyCache
+    L, T, k, B = 9000, 6, 256, 1024
+    K, Q, W = _inputs(L + 3, T, seed=21)
+    rng = np.random.default_rng(0)
+    paged = PagedKeyCache(128, B, n_pages=16, page_order=rng.permutation(16))
+    flat = PooledKeyCache(128, B, capacity=16 * B)
+    for c in (paged, flat):
+        c.append(K[:5000])
+        c.append(K[5000:L])
+    kw = dict(budget_k=k, active_heads_h=8, block_size=B)
+    a = IndexerEngine(method, **kw).decode(queries=Q, weights=W, cache=paged)
+    b = IndexerEngine(method, **kw).decode(queries=Q, weights=W, cache=flat)
+    torch.cuda.synchronize()
+    assert torch.equal(a.topk, b.topk)
+    if method != "dsa":
+        assert torch.equal(a.heads, b.heads)
+    for i in range(L, L + 3):  # token-by-token appends
+        paged.append(K[i:i + 1])
+        flat.append(K[i:i + 1])
+    a = IndexerEngine(method, **kw).decode(queries=Q, weights=W, cache=paged)
+    b = IndexerEngine(method, **kw).decode(queries=Q, weights=W, cache=flat)
+    torch.cuda.synchronize()
+    assert torch.equal(a.topk, b.topk)
+
+
+def test_decode_graph_over_paged_cache():
+    """DecodeGraph replay over a PagedKeyCache (page-bucketed capture) == eager paged decode."""
+    from paper_2605_07363_b200 import DecodeGraph, IndexerEngine, PagedKeyCache
+    L0, T, k, B = 5000, 2, 256, 1024
+    K, Q, W = _inputs(L0 + 1100, T * 3, seed=23)
+    rng = np.random.default_rng(1)
+    cache = PagedKeyCache(128, B, n_pages=8, page_order=rng.permutation(8))
+    cache.append(K[:L0])
+    dg = DecodeGraph(IndexerEngine("misa", budget_k=k, active_heads_h=8, block_size=B), cache, T, 64)
+    for step, L in enumerate((L0, L0 + 500, L0 + 1100)):  # crosses a page boundary (re-capture)
+        if cache.length < L:
+            cache.append(K[cache.length:L])
+        q, w = Q[step * T:(step + 1) * T], W[step * T:(step + 1) * T]
+        got = dg.step(q, w)
+        ref = IndexerEngine("misa", budget_k=k, active_heads_h=8, block_size=B).decode(queries=q, weights=w,
+                                                                                       cache=cache)
+        torch.cuda.synchronize()
+        assert torch.equal(got.topk, ref.topk) and torch.equal(got.heads, ref.heads), L
