@@ -212,14 +212,18 @@ __global__ void __launch_bounds__(192, 1)
         ptx::tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * 128;
         const int lim = nf - chunk * 128;  // valid columns for this row
+        // four independent partial sums (column i -> sum i % 4): the epilogue is latency-bound
+        // with one warp per SM sub-partition, so the add chain must not be serial
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};
         for (int c = 0; c < ncols; c += 32) {  // ncols is uniform per item
           uint32_t r[32];
           ptx::tmem_ld_x32(taddr + c, r);
           ptx::tmem_wait_ld_dep(r);
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (c + i < lim) sum += fmaxf(__uint_as_float(r[i]), 0.f);
+            if (c + i < lim) ps[i & 3] += fmaxf(__uint_as_float(r[i]), 0.f);
         }
+        sum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }
@@ -230,18 +234,19 @@ __global__ void __launch_bounds__(192, 1)
       if (t < a.T && chunk == 0 && rem > 0) {
         const uint8_t* qa = sA + s * C::A_BYTES;
         const float4* pv = reinterpret_cast<const float4*>(sP + (s * C::P_ROWS + (lrow >> a.hp_log2)) * D);
-        float dot = 0.f;
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;  // four independent FMA chains
 #pragma unroll 4
         for (int c = 0; c < D / 8; ++c) {
           const uint4 u = *reinterpret_cast<const uint4*>(qa + ptx::sw128_offset(lrow, c * 8, C::A_ATOM));
           const float4 p0 = pv[2 * c], p1 = pv[2 * c + 1];
           const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
           float2 f;
-          f = __bfloat1622float2(h[0]); dot = fmaf(f.x, p0.x, dot); dot = fmaf(f.y, p0.y, dot);
-          f = __bfloat1622float2(h[1]); dot = fmaf(f.x, p0.z, dot); dot = fmaf(f.y, p0.w, dot);
-          f = __bfloat1622float2(h[2]); dot = fmaf(f.x, p1.x, dot); dot = fmaf(f.y, p1.y, dot);
-          f = __bfloat1622float2(h[3]); dot = fmaf(f.x, p1.z, dot); dot = fmaf(f.y, p1.w, dot);
+          f = __bfloat1622float2(h[0]); d0 = fmaf(f.x, p0.x, d0); d0 = fmaf(f.y, p0.y, d0);
+          f = __bfloat1622float2(h[1]); d1 = fmaf(f.x, p0.z, d1); d1 = fmaf(f.y, p0.w, d1);
+          f = __bfloat1622float2(h[2]); d2 = fmaf(f.x, p1.x, d2); d2 = fmaf(f.y, p1.y, d2);
+          f = __bfloat1622float2(h[3]); d3 = fmaf(f.x, p1.z, d3); d3 = fmaf(f.y, p1.w, d3);
         }
+        const float dot = (d0 + d1) + (d2 + d3);
         sum += fmaxf(dot / (float)rem, 0.f);
       }
       ptx::mbar_arrive(&empty_a[s]);
