@@ -323,3 +323,31 @@ def test_virtual_key_shards_merge_to_single_gpu_result(method, G):
               stream)
     torch.cuda.synchronize()
     assert torch.equal(out[:L], ref)
+
+
+@pytest.mark.parametrize("method,H,h,d,B,k", [
+    ("misa", 64, 8, 128, 1024, 2048),   # headline shape (pair TMEM layout)
+    ("misa", 16, 4, 64, 256, 64),       # d = 64, small k (smallest compiled selector capacity)
+    ("misa", 32, 16, 128, 512, 512),    # 16 routed heads: query-major epilogue
+    ("dsa", 128, 8, 128, 1024, 1024),   # 128 heads: 8-warp epilogue
+    ("misa", 64, 32, 64, 64, 4096),     # k >= 4096: stride-16 sample, 512-thread selector
+    ("misa_hier", 64, 8, 128, 1024, 512),
+])
+def test_prefill_selector_equals_decode_selector(method, H, h, d, B, k):
+    """Two independent exact selection paths over the same scores must agree row for row:
+    the fused prefill filter + candidate selector and the decode path (key-split dense
+    scores + long-row selector)."""
+    from paper_2605_07363_b200 import IndexerEngine
+    gen = torch.Generator(device="cuda").manual_seed(31)
+    L = 20000
+    K = torch.randn(L, d, device="cuda", generator=gen).bfloat16()
+    Q = torch.randn(L, H, d, device="cuda", generator=gen).bfloat16()
+    W = torch.softmax(torch.randn(L, H, device="cuda", generator=gen), -1).float()
+    kw = dict(budget_k=k, active_heads_h=h, block_size=B, candidate_kprime=max(2048, 2 * k))
+    pre = IndexerEngine(method, **kw).run(K, Q, W)
+    rows = torch.tensor([0, 63, 64, 65, 2047, 2048, 5000, 12345, L - 2, L - 1], device="cuda")
+    dec = IndexerEngine(method, **kw).decode(K, Q[rows], W[rows], prefix_len=(rows + 1).cpu().numpy())
+    torch.cuda.synchronize()
+    assert torch.equal(dec.topk, pre.topk[rows]), method
+    if method != "dsa":
+        assert torch.equal(dec.heads, pre.heads[rows])
