@@ -1021,15 +1021,11 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nc[j];
     // no candidates needed: every prefix token (n <= k) or an empty prefix (counts unset)
     if ((nx_n <= k && !want_scores) || nx_n <= 0) return;
-    uint32_t bytes = 0;
-#pragma unroll
-    for (int j = 0; j < kQuadrants; ++j) bytes += ((min(max(nc[j], 0), cap) * 8u) + 15u) & ~15u;
+    // the row's four lists are one contiguous region: a single bulk copy of all of it
+    // (a cheap issue beats copying only the ~2/3 that is filled)
+    const uint32_t bytes = kQuadrants * cap * 8u;
     ptx::mbar_arrive_expect_tx(&mbar, bytes);
-#pragma unroll
-    for (int j = 0; j < kQuadrants; ++j) {
-      const uint32_t b = ((min(max(nc[j], 0), cap) * 8u) + 15u) & ~15u;
-      if (b) ptx::bulk_g2s(raw + (size_t)j * cap, cand + ((int64_t)row * kQuadrants + j) * cap, b, &mbar);
-    }
+    ptx::bulk_g2s(raw, cand + (int64_t)row * kQuadrants * cap, bytes, &mbar);
     pf.copy = true;
   };
   if (tid == 0) {
@@ -1112,13 +1108,13 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
       sh.rmax[w] = mx;
     }
     for (int i = tid; i < 2048; i += NT) sh.hist[i] = 0u;
-    __syncthreads();  // raw consumed: start the next row's copy
+    __syncthreads();  // raw consumed: the next row's copy may start
     SEL_MARK(ti_, 2);
-    if (tid == 0) {
-      issue(t + gridDim.x);
-      load_meta(t + 2 * gridDim.x);
-    }
     if (overflow || total < kk) {
+      if (tid == 0) {
+        issue(t + gridDim.x);
+        load_meta(t + 2 * gridDim.x);
+      }
       for (int i = tid; i < k; i += NT) out[i] = -1;
       if (tid == 0 && flags) flags[t] = overflow ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
       __syncthreads();  // pf (next row) published before anyone reads it
@@ -1174,6 +1170,12 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     }
     __syncthreads();
     SEL_MARK(ti_, 5);
+    // start the next row's copy here rather than right after extraction: the issuing
+    // thread's delay then overlaps the chunk scan instead of stalling the cut's barriers
+    if (tid == 0) {
+      issue(t + gridDim.x);
+      load_meta(t + 2 * gridDim.x);
+    }
     SEL_MARK(ti_, 6);
     // ---- exclusive scan of the chunk histogram (in place)
     {
