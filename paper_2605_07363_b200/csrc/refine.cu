@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
           }
           const float sc = gate_relu_finish(s0, s1);
           const int i = j * 128 + quad * 32 + lane;
-          if (i < nc) a.out[(int64_t)t * a.out_ld + i] = sc;
+          if (i < nc) __stcs(a.out + (int64_t)t * a.out_ld + i, sc);  // streaming: keep L2 for the keys
         }
       }
       __syncwarp();
