@@ -380,22 +380,23 @@ class IndexerEngine:
         return int(bad.numel())
 
     def _dense_rows(self, x: PreparedInputs, heads, hq, k, out, rows: np.ndarray, scores=None):
-        """Exact fallback: materialize full score rows for the flagged rows' groups, dense select."""
+        """Exact fallback for flagged rows: the decode machinery on just those rows (their
+        queries / gates / heads gathered), i.e. key-split dense scores on every SM and the
+        long-row exact selector — one pass for all flagged rows, whatever their number."""
         dev = x.keys.device
-        G = 256 // hq
-        stream = self._stream()
-        scratch = self._buf("dense_scratch", (G, x.L), torch.float32, dev)
-        for g in np.unique(rows // G):
-            r0 = int(g) * G
-            nmax = int(x.prefix_host[r0:r0 + G].max())
-            items = torch.tensor([g], dtype=torch.int32, device=dev)
-            tiles = torch.tensor([(nmax + 127) // 128], dtype=torch.int32, device=dev)
-            base = scratch.data_ptr() - r0 * x.L * 4  # row t of the group lands in scratch[t - r0]
-            _lib.call("misa_score_materialize", _ptr(x.keys), x.L, 1, x.D, _ptr(x.queries), _ptr(x.weights), x.H,
-                      x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles), 1, base, x.L, stream)
-            sel = torch.from_numpy(rows[(rows // G) == g].astype(np.int32)).to(dev)
-            _lib.call("misa_select_dense", base, x.L, None, 0, _ptr(x.prefix), _ptr(sel), sel.numel(), k, _ptr(out),
-                      out.stride(0), _ptr(scores), stream)
+        sel = torch.from_numpy(rows.astype(np.int64)).to(dev)
+        xr = PreparedInputs(x.keys, x.queries.index_select(0, sel).contiguous(),
+                            x.weights.index_select(0, sel).contiguous(), x.prefix.index_select(0, sel).contiguous(),
+                            x.prefix_host[rows], x.L, int(rows.shape[0]), x.H, x.Hp, x.d, x.D, None, x.pages)
+        if heads is not None and heads.dim() == 1:  # a raw workspace buffer
+            heads = heads[: x.T * hq].view(x.T, hq)
+        hr = None if heads is None else heads.index_select(0, sel).contiguous()
+        o = torch.empty((xr.T, k), dtype=torch.int32, device=dev)
+        so = None if scores is None else torch.empty((xr.T, k), dtype=torch.float32, device=dev)
+        self.dense_select(xr, hr, hq, k, o, scores=so)
+        out[sel] = o
+        if scores is not None:
+            scores[sel] = so
 
     def refine(self, x: PreparedInputs, cand: torch.Tensor, k: int, out: torch.Tensor):
         """K5 + dense select within candidates (MISA-dagger fine stage)."""
