@@ -444,6 +444,135 @@ __global__ void __launch_bounds__(NT, (NT * EPT <= 4096 ? 6 : 1)) threshold_kern
   }
 }
 
+// Warp-per-row variant (samples per row <= 16384): no block barriers, a private 2048-bin
+// histogram per warp, 24 rows per SM in flight; same windows and rounding as above, so
+// tau is identical.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) threshold_warp_kernel(
+    const float* __restrict__ s, int64_t ld, const int32_t* __restrict__ prefix_len, int n_rows, int stride, int k,
+    float beta, int64_t append_all, float* __restrict__ tau, int elem_step) {
+  constexpr int NB = 2048;
+  __shared__ uint32_t hist_all[WARPS][NB];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t* hist = hist_all[w];
+  for (int t = blockIdx.x * WARPS + w; t < n_rows; t += gridDim.x * WARPS) {
+    const int n = prefix_len[t];
+    if (n <= append_all || n <= k) {
+      if (lane == 0) tau[t] = -INFINITY;
+      continue;
+    }
+    const int m = (n + stride - 1) / stride;
+    long long jj = (long long)ceilf(beta * (float)k * (float)m / (float)n);
+    jj = jj < 1 ? 1 : (jj > m ? m : jj);
+    const float* row = s + (int64_t)t * ld;
+    // visit(fn): fn(key) for every sample of the row; 16-byte loads, 16 per lane in flight
+    const bool vec = elem_step == 1 && ((reinterpret_cast<uintptr_t>(row) & 15) == 0);
+    auto visit = [&](auto&& fn) {
+      int done = 0;
+      if (vec) {
+        const int m4 = m >> 2;
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        for (int v0 = lane; v0 < m4; v0 += 32 * 4) {
+          float4 x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = v0 + 32 * u < m4 ? __ldg(r4 + v0 + 32 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (v0 + 32 * u < m4) {
+              fn(float_key(x[u].x));
+              fn(float_key(x[u].y));
+              fn(float_key(x[u].z));
+              fn(float_key(x[u].w));
+            }
+        }
+        done = m4 << 2;
+      }
+      for (int e0 = done + lane; e0 < m; e0 += 32 * 8) {
+        uint32_t kv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) kv[u] = e0 + 32 * u < m ? float_key(row[(int64_t)(e0 + 32 * u) * elem_step]) : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + 32 * u < m) fn(kv[u]);
+      }
+    };
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    visit([&](uint32_t kv) {
+      mn = min(mn, kv);
+      mx = max(mx, kv);
+    });
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    bool narrow = mx - mn > (1u << 24);
+    uint32_t lo = narrow ? mx - (1u << 24) : mn;
+    uint32_t span = mx - lo;
+    int sft = span == 0u ? 0 : max(0, 32 - __clz(span) - 11);
+    int above_prev = 0;
+    for (int level = 0;; ++level) {
+      for (int i = lane * 4; i < NB; i += 128) *reinterpret_cast<uint4*>(hist + i) = make_uint4(0u, 0u, 0u, 0u);
+      __syncwarp();
+      visit([&](uint32_t kv) {
+        const uint32_t d = kv - lo;
+        if (kv >= lo && d <= span) atomicAdd(&hist[d >> sft], 1u);
+      });
+      __syncwarp();
+      // lane owns bins [NB - 64(lane+1), NB - 64 lane) (descending keys)
+      const int b0 = NB - 64 * (lane + 1);
+      int cnt = 0;
+#pragma unroll 4
+      for (int i = 0; i < 64; i += 4) {
+        const uint4 h4 = *reinterpret_cast<const uint4*>(hist + b0 + i);
+        cnt += (int)(h4.x + h4.y + h4.z + h4.w);
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int ex = above_prev + incl - cnt;
+      const bool mine = ex < jj && jj <= ex + cnt;
+      const uint32_t who = __ballot_sync(0xffffffffu, mine);
+      if (who == 0u) {  // the j-th sample is below the narrow window: whole range
+        narrow = false;
+        lo = mn;
+        span = mx - mn;
+        sft = span == 0u ? 0 : max(0, 32 - __clz(span) - 11);
+        above_prev = 0;
+        level = -1;
+        __syncwarp();
+        continue;
+      }
+      const int src = __ffs(who) - 1;
+      int B = 0, A = 0;
+      if (lane == src) {
+        int a = ex;
+        for (int i = 63; i >= 0; --i) {
+          const int h = (int)hist[b0 + i];
+          if (a < jj && jj <= a + h) {
+            B = b0 + i;
+            A = a;
+            break;
+          }
+          a += h;
+        }
+      }
+      B = __shfl_sync(0xffffffffu, B, src);
+      A = __shfl_sync(0xffffffffu, A, src);
+      lo += (uint32_t)B << sft;
+      __syncwarp();
+      if (narrow || level == 1 || sft <= 12) {
+        if (lane == 0) tau[t] = key_float(lo);  // lower edge of the bin: <= the j-th sample
+        break;
+      }
+      span = (1u << sft) - 1u;
+      sft = sft - 11;
+      above_prev = A;  // samples above the refined window
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------- v3 row selector core ----
 // Warp w owns the contiguous element range [w*WE, (w+1)*WE) of the row's
 // concatenated lists (WE = 32*EPT); lane l's slot r is element w*WE + 32r + l.
@@ -1694,17 +1823,6 @@ static unsigned persistent_grid(K kern, int nt, int64_t rows, bool persistent = 
 }
 
 template <int NT, int EPT>
-struct ThresholdL {
-  static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
-                float beta, int64_t aa, float* tau) {
-    threshold_kernel<NT, EPT><<<persistent_grid(threshold_kernel<NT, EPT>, NT, T, NT * EPT <= 4096), NT, 0, st>>>(
-        s, ld, pl, (int)T, stride, k, beta, aa, tau);
-    MISA_LAUNCH_CHECK();
-    return MISA_OK;
-  }
-};
-
-template <int NT, int EPT>
 struct ThresholdStepL {  // samples every `stride`-th element of a dense row
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* pl, int64_t T, int stride, int k,
                 float beta, int64_t aa, float* tau) {
@@ -1801,10 +1919,16 @@ extern "C" int misa_select_threshold(const float* sample_scores, int64_t ld, con
                                      float* tau, void* stream) {
   MISA_REQUIRE(sample_scores && prefix_len && tau, "null pointer");
   MISA_REQUIRE(k >= 1 && key_stride >= 1 && beta > 0.f && n_rows >= 1, "bad threshold arguments");
-  const int rc = dispatch_capacity<ThresholdL>(ld, as_stream(stream), sample_scores, ld, prefix_len, n_rows,
-                                               key_stride, k, beta, append_all_len, tau);
-  MISA_REQUIRE(rc != -100, "sample row length %lld exceeds the register selector (16384)", (long long)ld);
-  return rc;
+  // one warp per row: 32 KB of histograms per 4-warp CTA, 6 CTAs (24 rows) per SM
+  constexpr int WARPS = 4;
+  auto kern = threshold_warp_kernel<WARPS>;
+  int per_sm = 0;
+  MISA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, 0));
+  const int64_t grid = std::min<int64_t>((n_rows + WARPS - 1) / WARPS, (int64_t)sm_count() * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, WARPS * 32, 0, as_stream(stream)>>>(sample_scores, ld, prefix_len, (int)n_rows, key_stride,
+                                                              k, beta, append_all_len, tau, 1);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
 }
 
 extern "C" int misa_select_topk(const uint64_t* cand, const int32_t* cand_count, int cap, const int32_t* prefix_len,

@@ -262,6 +262,35 @@ def test_threshold_and_filter_select_roundtrip():
     assert (tot[big] <= 4 * cap).all() and (tot[big] >= k).all()
 
 
+@pytest.mark.parametrize("spread", [1.0, 1e6])
+def test_threshold_bounds_jth_sample(spread):
+    """tau <= the j-th largest sample (j = ceil(beta*k*m/n)) and lies within one histogram bin of it."""
+    torch.manual_seed(8)
+    T, n_max, stride, k, beta = 70, 300000, 32, 2048, 2.0
+    m_max = (n_max + stride - 1) // stride
+    samp = torch.randn(T, m_max, device="cuda") * spread
+    samp[1::3, :7] = 1e30  # a few huge outliers: the j-th sample falls below the narrow window
+    samp[2] = 0.5  # all ties
+    prefix = torch.randint(k + 1, n_max + 1, (T,), dtype=torch.int32, device="cuda")
+    prefix[0] = k  # <= k -> -inf
+    tau = torch.empty(T, device="cuda")
+    _lib().call("misa_select_threshold", _p(samp), m_max, _p(prefix), T, stride, k, beta, 0, _p(tau), _stream())
+    torch.cuda.synchronize()
+    assert tau[0].item() == float("-inf")
+    def key(x):  # the order-preserving uint32 key of csrc/ptx.cuh float_key
+        u = int(np.float32(x).view(np.uint32))
+        return u ^ (0xFFFFFFFF if u >> 31 else 0x80000000)
+
+    for t in range(1, T):
+        n = int(prefix[t])
+        m = (n + stride - 1) // stride
+        j = min(max(int(np.ceil(np.float32(beta) * np.float32(k) * np.float32(m) / np.float32(n))), 1), m)
+        row = samp[t, :m]
+        jth = torch.sort(row, descending=True).values[j - 1]
+        assert tau[t] <= jth, (t, tau[t].item(), jth.item())
+        assert key(jth.item()) - key(tau[t].item()) < (1 << 14), t  # narrow window: 2^24 / 2^10.. bins
+
+
 def test_merge_topk():
     torch.manual_seed(6)
     T, k, parts = 33, 40, 3
