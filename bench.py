@@ -57,7 +57,9 @@ def _args():
     p.add_argument("--kprime", type=int, default=8192)
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--hier", action="store_true", help="also time MISA-dagger (k'=--kprime)")
+    p.add_argument("--no-hier", action="store_true", help="skip timing MISA-dagger (k'=--kprime)")
+    p.add_argument("--hier", action="store_true", help=argparse.SUPPRESS)  # the default now
+    p.add_argument("--no-needle", action="store_true", help="skip the needle-retrieval recall leg")
     p.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
     p.add_argument("--no-sweep", action="store_true", help="skip the C2 / C3 prefill configs")
     return p.parse_args()
@@ -295,7 +297,7 @@ def run_ours(a):
 
     hier_ms = None
     hstages = {}
-    if a.hier and world == 1:
+    if not a.no_hier and world == 1:
         eng_h = IndexerEngine("misa_hier", budget_k=a.k, active_heads_h=a.h, block_size=a.B,
                               candidate_kprime=a.kprime)
         hier_ms = _time_steps(lambda: eng_h.run_prepared(x), a.steps, a.warmup, barrier)
@@ -416,6 +418,12 @@ def run_ours(a):
                           "eager engine.decode and CUDA-graph DecodeGraph replay, ms per step",
                   "rows": decode_numbers()}
 
+    needle = None
+    if world == 1 and not a.no_needle:
+        sys.path.insert(0, os.path.join(REPO, "tools"))
+        from needle_bench import needle_numbers
+        needle = needle_numbers(L=L, k=a.k, h=a.h, B=a.B, kprime=a.kprime)
+
     line = {
         "metric": METRIC, "value": round(misa_ms, 3), "unit": "ms/layer", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(misa_ms, 3), "higher_is_better": False,
@@ -432,7 +440,7 @@ def run_ours(a):
         "dsa_stages_ms": {k: round(v, 4) for k, v in dstages.items()},
         "fallback_rows": fallback,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
-        "decode": decode, "sharded_decode": sdec, "configs": sweep,
+        "decode": decode, "sharded_decode": sdec, "configs": sweep, "needle": needle,
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)

@@ -130,3 +130,22 @@ def test_select_batch_host_pipeline_equals_device_path():
     dev = est.select_batch(K.cuda(), Q.cuda(), W.cuda()).topk
     torch.cuda.synchronize()
     assert not host.is_cuda and torch.equal(host, dev.cpu())
+
+
+def test_constructive_needle_retrieval():
+    """Acceptance criterion 5 (``test_acceptance.py:203-243``) through the GPU registry:
+    margin-10, 32-token needles aligned with the top-gate head are fully retrieved by the
+    dense, routed and hierarchical indexers at every length and depth of the reference grid."""
+    from paper_2605_07363_b200 import IndexerConfig, gen_needle_workload, make_indexer, needle_recall
+    cfg = IndexerConfig()
+    misses = []
+    for li, L in enumerate((1024, 2048, 4096, 8192)):
+        k = min(cfg.budget_k, L // 4)
+        idx = {m: make_indexer(m, budget_k=k) for m in ("dsa", "misa", "misa_hier")}
+        for di in range(11):
+            for rep in range(2):
+                w = gen_needle_workload(1000 * li + 10 * di + rep, L, di / 10, 32, 10.0, cfg, noise_scale=0.01)
+                for m, ix in idx.items():
+                    if needle_recall(ix.select(w).selection, w.label.interval) < 1.0:
+                        misses.append((m, L, di, rep))
+    assert not misses, misses[:5]

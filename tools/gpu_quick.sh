@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 python -m paper_2605_07363_b200._build > /dev/null
 timeout 600 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --no-cpu --no-e2e --no-decode --no-sweep --steps 5 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python bench.py --no-cpu --no-e2e --no-decode --no-sweep --no-needle --steps 5 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
 tail -3 gpurun_out/bench.err; cat gpurun_out/pytest_gpu.log
 python - <<'PY'
 import json
