@@ -58,6 +58,23 @@ struct RouteCfg {
 
 __device__ __forceinline__ int route_item(int it, int P, int b) { return (it & 1) ? (it + 1) * P - 1 - b : it * P + b; }
 
+// A work item's metadata, loaded one item ahead by every role: each role walks the same
+// item list and would otherwise pay a dependent global-load round trip per tile.
+struct RouteItem {
+  int idx, chunk, ncols, tile;
+};
+__device__ __forceinline__ RouteItem load_route_item(const RouteArgs& a, int it, int P, int b) {
+  RouteItem m;
+  m.idx = route_item(it, P, b);
+  m.chunk = m.ncols = m.tile = 0;
+  if (m.idx < a.n_items) {
+    m.chunk = __ldg(a.it_chunk + m.idx);
+    m.ncols = __ldg(a.it_ncols + m.idx);
+    m.tile = __ldg(a.it_tile + m.idx);
+  }
+  return m;
+}
+
 template <int D>
 __global__ void __launch_bounds__(192, 1)
     route_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_p,
@@ -103,59 +120,66 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (ptx::elect_one()) {
-      int s = 0, cur_chunk = -1, nb = 0;
-      uint32_t ph = 0;
-      for (int it = 0;; ++it) {
-        const int idx = route_item(it, P, bid);
-        if (idx >= a.n_items) break;
-        const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
-        if (ncols == 0 && chunk != 0) continue;
-        if (ncols > 0 && chunk != cur_chunk) {
+    // the whole warp produces: lane rr owns query row rr of the tile (<= 16 rows) and
+    // stages its partial-block prefix row; lane 0 issues the tile loads
+    const int rows = 128 >> a.hp_log2;
+    auto row_n = [&](const RouteItem& m) {
+      const int t = m.tile * rows + lane;
+      return (m.idx < a.n_items && lane < rows && t < a.T) ? __ldg(a.prefix_len + t) : 0;
+    };
+    int s = 0, cur_chunk = -1, nb = 0;
+    uint32_t ph = 0;
+    RouteItem nx = load_route_item(a, 0, P, bid);
+    int nx_n = row_n(nx);
+    for (int it = 0;; ++it) {
+      const RouteItem cu = nx;
+      const int n = nx_n;
+      if (cu.idx >= a.n_items) break;
+      nx = load_route_item(a, it + 1, P, bid);
+      nx_n = row_n(nx);
+      const int chunk = cu.chunk, ncols = cu.ncols, tile = cu.tile;
+      if (ncols == 0 && chunk != 0) continue;
+      if (ncols > 0 && chunk != cur_chunk) {
+        if (lane == 0) {
           if (nb > 0) ptx::mbar_wait(bempty, (nb - 1) & 1);
           ptx::mbar_arrive_expect_tx(bfull, C::B_BYTES);
           for (int p = 0; p < 3; ++p)
             for (int at = 0; at < D / 64; ++at)
               ptx::tma_load_2d(sB + p * C::B_PLANE + at * C::B_ATOM, &tmap_p, bfull, at * 64,
                                (int)(p * a.planes_rows + chunk * 128));
-          cur_chunk = chunk;
-          ++nb;
         }
-        // chunk 0 also stages each row's partial-block prefix sum P[n-1] for the epilogue
-        const int rows = 128 >> a.hp_log2;
-        int np = 0;
-        if (chunk == 0)
-          for (int rr = 0; rr < rows; ++rr) {
-            const int t = a.it_tile[idx] * rows + rr;
-            if (t < a.T && a.prefix_len[t] % a.B) ++np;
-          }
+        cur_chunk = chunk;
+        ++nb;
+      }
+      // chunk 0 also stages each row's partial-block prefix sum P[n-1] for the epilogue
+      const bool part = chunk == 0 && n % a.B != 0;  // n == 0 (padding rows) -> false
+      const int np = __popc(__ballot_sync(0xffffffffu, part));
+      if (lane == 0) {
         ptx::mbar_wait(&empty_a[s], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES + np * D * 4);
         for (int at = 0; at < D / 64; ++at)
-          ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_q, &full_a[s], at * 64, a.it_tile[idx] * 128);
-        if (np)
-          for (int rr = 0; rr < rows; ++rr) {
-            const int t = a.it_tile[idx] * rows + rr;
-            const int n = t < a.T ? a.prefix_len[t] : 0;
-            if (t < a.T && n % a.B)
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                      ptx::smem_u32(sP + (s * C::P_ROWS + rr) * D)),
-                  "l"(a.prefix + (int64_t)(n - 1) * D), "r"(D * 4), "r"(ptx::smem_u32(&full_a[s]))
-                  : "memory");
-          }
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+          ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_q, &full_a[s], at * 64, tile * 128);
       }
+      __syncwarp();  // stage s is free (lane 0 waited on it) before any lane writes it
+      if (part)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                ptx::smem_u32(sP + (s * C::P_ROWS + lane) * D)),
+            "l"(a.prefix + (int64_t)(n - 1) * D), "r"(D * 4), "r"(ptx::smem_u32(&full_a[s]))
+            : "memory");
+      if (++s == STAGES) { s = 0; ph ^= 1; }
     }
   } else if (warp == 1) {
     if (ptx::elect_one()) {
       int s = 0, acc = 0, cur_chunk = -1, nb = 0;
       uint32_t ph = 0, aph = 0;
       const uint32_t b_base = ptx::smem_u32(sB);
+      RouteItem nx = load_route_item(a, 0, P, bid);
       for (int it = 0;; ++it) {
-        const int idx = route_item(it, P, bid);
-        if (idx >= a.n_items) break;
-        const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
+        const RouteItem cu = nx;
+        if (cu.idx >= a.n_items) break;
+        nx = load_route_item(a, it + 1, P, bid);
+        const int chunk = cu.chunk, ncols = cu.ncols;
         if (ncols == 0 && chunk != 0) continue;
         if (ncols == 0) {  // partial-block-only tile: no MMA, just hand the stage back
           ptx::mbar_wait(&full_a[s], ph);
@@ -195,41 +219,29 @@ __global__ void __launch_bounds__(192, 1)
     const int quad = warp & 3;
     int acc = 0, s = 0;
     uint32_t aph = 0, ph = 0;
+    const int lrow = quad * 32 + lane;  // A tile row = (t, j) pair
+    auto row_len = [&](const RouteItem& m) {
+      const int tt = (int)(((int64_t)m.tile * 128 + lrow) >> a.hp_log2);
+      return (m.idx < a.n_items && tt < a.T) ? __ldg(a.prefix_len + tt) : 0;
+    };
+    RouteItem nx = load_route_item(a, 0, P, bid);
+    int nx_n = row_len(nx);
     for (int it = 0;; ++it) {
-      const int idx = route_item(it, P, bid);
-      if (idx >= a.n_items) break;
-      const int chunk = a.it_chunk[idx], ncols = a.it_ncols[idx];
+      const RouteItem cu = nx;
+      const int n = nx_n;
+      if (cu.idx >= a.n_items) break;
+      nx = load_route_item(a, it + 1, P, bid);
+      nx_n = row_len(nx);
+      const int chunk = cu.chunk, ncols = cu.ncols;
       if (ncols == 0 && chunk != 0) continue;
-      const int lrow = quad * 32 + lane;  // A tile row = (t, j) pair
-      const int64_t grow = (int64_t)a.it_tile[idx] * 128 + lrow;
+      const int64_t grow = (int64_t)cu.tile * 128 + lrow;
       const int t = (int)(grow >> a.hp_log2);
       const int j = (int)(grow & (a.Hp - 1));
-      const int n = t < a.T ? a.prefix_len[t] : 0;
       const int nf = n / a.B;
-      float sum = 0.f;
-      if (ncols > 0) {
-        ptx::mbar_wait(&tfull[acc], aph);
-        ptx::tc_fence_after();
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * 128;
-        const int lim = nf - chunk * 128;  // valid columns for this row
-        // four independent partial sums (column i -> sum i % 4): the epilogue is latency-bound
-        // with one warp per SM sub-partition, so the add chain must not be serial
-        float ps[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int c = 0; c < ncols; c += 32) {  // ncols is uniform per item
-          uint32_t r[32];
-          ptx::tmem_ld_x32(taddr + c, r);
-          ptx::tmem_wait_ld_dep(r);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c + i < lim) ps[i & 3] += fmaxf(__uint_as_float(r[i]), 0.f);
-        }
-        sum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
-      }
-      // partial last block: mean over keys [nf*B, n) = P[n-1] / rem, with q from the A stage
+      // partial last block first (it needs only the A stage, not the MMA): mean over keys
+      // [nf*B, n) = P[n-1] / rem, with q from the A stage
       ptx::mbar_wait(&full_a[s], ph);
+      float sum = 0.f;
       const int rem = n - nf * a.B;
       if (t < a.T && chunk == 0 && rem > 0) {
         const uint8_t* qa = sA + s * C::A_BYTES;
@@ -247,7 +259,37 @@ __global__ void __launch_bounds__(192, 1)
           f = __bfloat1622float2(h[3]); d3 = fmaf(f.x, p1.z, d3); d3 = fmaf(f.y, p1.w, d3);
         }
         const float dot = (d0 + d1) + (d2 + d3);
-        sum += fmaxf(dot / (float)rem, 0.f);
+        sum = fmaxf(dot / (float)rem, 0.f);
+      }
+      if (ncols > 0) {
+        ptx::mbar_wait(&tfull[acc], aph);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * 128;
+        const int lim = nf - chunk * 128;  // valid columns for this row
+        // every column slice in flight before one wait; four independent partial sums
+        // (column i -> sum i % 4): one warp per SM sub-partition, so nothing may be serial
+        uint32_t r[128];
+#pragma unroll
+        for (int c = 0; c < 128; c += 32)
+          if (c < ncols) ptx::tmem_ld_x32p(taddr + c, r + c);  // ncols is uniform per item
+#pragma unroll
+        for (int c = 0; c < 128; c += 32)
+          if (c < ncols) ptx::tmem_wait_ld_dep32p(r + c);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);  // accumulator drained: the next tile's MMA may start
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 128; c += 32)
+          if (c < ncols) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c + i < lim) ps[i & 3] += fmaxf(__uint_as_float(r[c + i]), 0.f);
+          }
+        // summation order: blocks in column order, then the partial block (as before: the
+        // partial block was added last)
+        const float full = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        sum = full + sum;
       }
       ptx::mbar_arrive(&empty_a[s]);
       if (++s == STAGES) { s = 0; ph ^= 1; }
