@@ -93,8 +93,11 @@ class PreparedInputs:
     pages: tuple | None = None  # paged key cache: (page_table (n_pages,) int32 device, page_size)
 
 
-def prepare_inputs(keys, queries, weights, prefix_len=None, device=None) -> PreparedInputs:
-    """Move/convert/pad inputs to the kernel layouts (no copy when already conforming)."""
+def prepare_inputs(keys, queries, weights, prefix_len=None, device=None, prefix_dev=None) -> PreparedInputs:
+    """Move/convert/pad inputs to the kernel layouts (no copy when already conforming).
+
+    ``prefix_dev``: the prefix lengths already on the device (int32, same values as
+    ``prefix_len``), so that no host->device copy is issued here."""
     dev = torch.device(device) if device is not None else (
         keys.device if isinstance(keys, torch.Tensor) and keys.is_cuda else torch.device("cuda"))
     K = torch.as_tensor(keys, device=dev)
@@ -136,7 +139,12 @@ def prepare_inputs(keys, queries, weights, prefix_len=None, device=None) -> Prep
             raise ValueError(f"prefix_len must have {T} entries")
         if host.min() < 1 or host.max() > L:
             raise ValueError("prefix lengths must lie in [1, L]")
-    prefix = torch.from_numpy(host.astype(np.int32)).to(dev)
+    if prefix_dev is not None:
+        if tuple(prefix_dev.shape) != (T,) or prefix_dev.dtype != torch.int32 or prefix_dev.device != K.device:
+            raise ValueError("prefix_dev must be a (T,) int32 tensor on the keys' device")
+        prefix = prefix_dev
+    else:
+        prefix = torch.from_numpy(host.astype(np.int32)).to(dev)
     return PreparedInputs(K, Q, W, prefix, host, L, T, H, Hp, d, D, causal_key)
 
 
@@ -366,6 +374,7 @@ class IndexerEngine:
                       _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(f_items), _ptr(f_tiles), f_items.numel(), _ptr(tau),
                       _ptr(cand), cap, _ptr(cnt), stream)
         flags = self._buf(tag + "_flags", (x.T,), torch.int32, dev)
+        self.last_flags = flags
         self._mark(tag + ":select")
         _lib.call("misa_select_topk", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, x.L, _ptr(out),
                   out.stride(0),
@@ -568,6 +577,11 @@ class IndexerEngine:
         spans = [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
         rmax = max(b - a for a, b in spans)
         comp = torch.cuda.current_stream()
+        # nothing in the loop below waits on the device: the prefix lengths go up once, and
+        # the fused selector's overflow flags are gathered on the device and checked after
+        # the last chunk (flagged rows are then re-run exactly from the host inputs)
+        pl_dev = torch.from_numpy(pl.astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+        flags_all = torch.zeros(T, dtype=torch.int32, device=dev)
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         Kd = torch.empty(Kh.shape, dtype=Kh.dtype, device=dev)
         Qd = [torch.empty((rmax,) + tuple(Qh.shape[1:]), dtype=Qh.dtype, device=dev) for _ in range(2)]
@@ -597,7 +611,14 @@ class IndexerEngine:
             comp.wait_event(ev_in[c])
             if c >= 2:
                 comp.wait_event(ev_out[c - 2])  # result buffer drained
-            self.run(Kd, Qd[buf][: b - a], Wd[buf][: b - a], prefix_len=pl[a:b], out=Od[buf][: b - a])
+            x = prepare_inputs(Kd, Qd[buf][: b - a], Wd[buf][: b - a], pl[a:b], prefix_dev=pl_dev[a:b])
+            check, self.check_overflow = self.check_overflow, False
+            try:
+                self.run_prepared(x, out=Od[buf][: b - a])
+            finally:
+                self.check_overflow = check
+            if check:
+                flags_all[a:b].copy_(self.last_flags[: b - a])
             ev_comp[c].record(comp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_comp[c])
@@ -605,6 +626,14 @@ class IndexerEngine:
                 ev_out[c].record(s_out)
         for e in ev_out:
             comp.wait_event(e)
+        if self.check_overflow:
+            bad = torch.nonzero(flags_all).flatten().cpu().numpy()
+            if bad.size:  # exact re-run of just those rows (the device path's own fallback)
+                torch.cuda.current_stream().synchronize()
+                bi = torch.from_numpy(bad)
+                fix = self.run(Kd, Qh[bi].to(dev), Wh[bi].to(dev), prefix_len=pl[bad]).topk
+                out[bi] = fix.cpu()
+            self.last_fallback_rows = int(bad.size)
         return out
 
     # ----------------------------------------------------------- entry

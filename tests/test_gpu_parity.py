@@ -287,6 +287,27 @@ def test_forced_fallback_rows_are_exact():
         assert res.topk[t].tolist() == list(range(256))
 
 
+@pytest.mark.parametrize("method", ["dsa", "misa", "misa_hier"])
+def test_host_pipeline_fallback_rows_are_exact(method):
+    """The copy-overlapped host pipeline checks the overflow flags once after the last
+    chunk; flagged rows (zero gates: every key ties) are re-run and come out exact."""
+    from paper_2605_07363_b200 import IndexerEngine
+    g = torch.Generator().manual_seed(5)
+    L, H = 12000, 8
+    K = torch.randn(L, 64, generator=g).bfloat16()
+    Q = torch.randn(L, H, 64, generator=g).bfloat16()
+    W = torch.softmax(torch.randn(L, H, generator=g), -1).float()
+    W[-5:] = 0.0
+    W[5000:5003] = 0.0  # flagged rows inside an early chunk as well
+    eng = IndexerEngine(method, budget_k=256, active_heads_h=4, block_size=64, candidate_kprime=1024)
+    host = eng.run_host(K.pin_memory(), Q.pin_memory(), W.pin_memory(), chunks=4)
+    assert eng.last_fallback_rows >= 8
+    dev = eng.run(K.cuda(), Q.cuda(), W.cuda()).topk.cpu()
+    assert torch.equal(host, dev)
+    for t in list(range(5000, 5003)) + list(range(L - 5, L)):
+        assert host[t].tolist() == list(range(256))
+
+
 @pytest.mark.parametrize("method,G", [("dsa", 2), ("misa", 4), ("dsa", 8)])
 def test_virtual_key_shards_merge_to_single_gpu_result(method, G):
     """Run every shard of a G-way key split on one GPU (local top-k with scores -> global
