@@ -1140,6 +1140,32 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
       nx_c4 = __ldg(reinterpret_cast<const int4*>(cand_count) + row);
     }
   };
+  // issue() = stage(): publish the row's (n, counts) in pf + launch(): its bulk copy.  On the
+  // common path they are split so that the issuing thread's dependent chain is short where
+  // it sits on the critical path (the chunk scan's barrier)
+  bool pend_copy = false;
+  int pend_row = 0;
+  auto stage = [&](int row) {
+    pf.row = row;
+    pf.copy = false;
+    pend_copy = false;
+    if (row >= n_rows) return;
+    pf.n = nx_n;
+    const int nc[kQuadrants] = {nx_c4.x, nx_c4.y, nx_c4.z, nx_c4.w};
+#pragma unroll
+    for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nc[j];
+    if ((nx_n <= k && !want_scores) || nx_n <= 0) return;
+    pf.copy = true;
+    pend_copy = true;
+    pend_row = row;
+  };
+  auto launch = [&]() {
+    if (!pend_copy) return;
+    const uint32_t bytes = kQuadrants * cap * 8u;
+    ptx::mbar_arrive_expect_tx(&mbar, bytes);
+    ptx::bulk_g2s(raw, cand + (int64_t)pend_row * kQuadrants * cap, bytes, &mbar);
+    pend_copy = false;
+  };
   auto issue = [&](int row) {
     pf.row = row;
     pf.copy = false;
@@ -1239,6 +1265,8 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     for (int i = tid; i < 2048; i += NT) sh.hist[i] = 0u;
     __syncthreads();  // raw consumed: the next row's copy may start
     SEL_MARK(ti_, 2);
+    const bool go = !(overflow || total < kk);
+    if (go && tid == 0) stage(t + gridDim.x);  // pf is free: every thread has read it
     if (overflow || total < kk) {
       if (tid == 0) {
         issue(t + gridDim.x);
@@ -1302,7 +1330,8 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
     // start the next row's copy here rather than right after extraction: the issuing
     // thread's delay then overlaps the chunk scan instead of stalling the cut's barriers
     if (tid == 0) {
-      issue(t + gridDim.x);
+      launch();
+      SEL_MARK(ti_, 14);
       load_meta(t + 2 * gridDim.x);
     }
     SEL_MARK(ti_, 6);

@@ -38,6 +38,8 @@ ok = (a[:, 8] > 0)
 print("rows", ok.sum(), "median cycles per phase:")
 for i, nm in enumerate(names[1:]):
     print(f"  {names[i]:>9s}->{nm:<9s} {int(np.median(d[ok, i])):8d}")
+if (a[ok, 14] > 0).any():
+    print("  issue only", int(np.median(a[ok, 14] - a[ok, 5])), " load_meta", int(np.median(a[ok, 6] - a[ok, 14])))
 print("  row total", int(np.median(a[ok, 8] - a[ok, 0])), " row-to-row", int(np.median(np.diff(a[ok, 0]))))
 cut = a[:, 9:14]
 okc = ok & (cut[:, 0] > 0) & (cut[:, 4] > 0)
