@@ -1130,58 +1130,53 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
   const int q = w / WPL;                       // this warp's quadrant list
   const int i0 = (w % WPL) * WE + lane;        // list position of slot 0 (slot r: i0 + 32r)
 
-  // (n, counts) of the row after next, loaded one row ahead of use into registers (one
-  // 16-byte load for the four counts; nothing waits on them until the next issue())
-  int nx_n = 0;
-  int4 nx_c4 = make_int4(0, 0, 0, 0);
+  // (n, counts) of the row after next, fetched one row ahead of use straight into shared
+  // memory with cp.async (registers are the scarce resource here: 512 threads x 2 CTAs)
+  __shared__ int4 meta_c;
+  __shared__ int meta_n;
   auto load_meta = [&](int row) {
     if (row < n_rows) {
-      nx_n = __ldg(prefix_len + row);
-      nx_c4 = __ldg(reinterpret_cast<const int4*>(cand_count) + row);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::smem_u32(&meta_n)), "l"(prefix_len + row)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(&meta_c)),
+                   "l"(cand_count + 4 * (int64_t)row)
+                   : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
   };
-  // issue() = stage(): publish the row's (n, counts) in pf + launch(): its bulk copy.  On the
-  // common path they are split so that the issuing thread's dependent chain is short where
-  // it sits on the critical path (the chunk scan's barrier)
-  bool pend_copy = false;
-  int pend_row = 0;
-  auto stage = [&](int row) {
+  auto publish = [&](int row) {  // pf <- the fetched (n, counts); true if the lists are needed
     pf.row = row;
     pf.copy = false;
-    pend_copy = false;
-    if (row >= n_rows) return;
-    pf.n = nx_n;
-    const int nc[kQuadrants] = {nx_c4.x, nx_c4.y, nx_c4.z, nx_c4.w};
-#pragma unroll
-    for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nc[j];
-    if ((nx_n <= k && !want_scores) || nx_n <= 0) return;
-    pf.copy = true;
-    pend_copy = true;
-    pend_row = row;
-  };
-  auto launch = [&]() {
-    if (!pend_copy) return;
-    const uint32_t bytes = kQuadrants * cap * 8u;
-    ptx::mbar_arrive_expect_tx(&mbar, bytes);
-    ptx::bulk_g2s(raw, cand + (int64_t)pend_row * kQuadrants * cap, bytes, &mbar);
-    pend_copy = false;
-  };
-  auto issue = [&](int row) {
-    pf.row = row;
-    pf.copy = false;
-    if (row >= n_rows) return;
-    pf.n = nx_n;
-    const int nc[kQuadrants] = {nx_c4.x, nx_c4.y, nx_c4.z, nx_c4.w};
-#pragma unroll
-    for (int j = 0; j < kQuadrants; ++j) pf.c[j] = nc[j];
+    if (row >= n_rows) return false;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const int nn = meta_n;
+    const int4 c4 = meta_c;
+    pf.n = nn;
+    pf.c[0] = c4.x;
+    pf.c[1] = c4.y;
+    pf.c[2] = c4.z;
+    pf.c[3] = c4.w;
     // no candidates needed: every prefix token (n <= k) or an empty prefix (counts unset)
-    if ((nx_n <= k && !want_scores) || nx_n <= 0) return;
-    // the row's four lists are one contiguous region: a single bulk copy of all of it
-    // (a cheap issue beats copying only the ~2/3 that is filled)
+    if ((nn <= k && !want_scores) || nn <= 0) return false;
+    pf.copy = true;
+    return true;
+  };
+  // the row's four lists are one contiguous region: a single bulk copy of all of it
+  // (a cheap issue beats copying only the ~2/3 that is filled)
+  auto copy_lists = [&](int row) {
     const uint32_t bytes = kQuadrants * cap * 8u;
     ptx::mbar_arrive_expect_tx(&mbar, bytes);
     ptx::bulk_g2s(raw, cand + (int64_t)row * kQuadrants * cap, bytes, &mbar);
-    pf.copy = true;
+  };
+  // issue() = stage() + launch().  On the common path they are split: stage() publishes pf
+  // right after extraction, launch() starts the copy later, where the issuing thread's
+  // chain is short on the critical path (the chunk scan's barrier)
+  auto stage = [&](int row) { publish(row); };
+  auto launch = [&]() {
+    if (pf.copy) copy_lists(pf.row);
+  };
+  auto issue = [&](int row) {
+    if (publish(row)) copy_lists(row);
   };
   if (tid == 0) {
     ptx::mbar_init(&mbar, 1);
@@ -1231,7 +1226,7 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
       overflow |= c[j] > cap;
       total += min(max(c[j], 0), cap);
     }
-    const int cq = min(max(c[q], 0), cap);
+    const int cq = min(max(q == 0 ? c[0] : q == 1 ? c[1] : q == 2 ? c[2] : c[3], 0), cap);  // no local array
     // slot rows of this warp that can hold list elements (warp-uniform)
     const int rv = EPT;  // unguarded: predicated slots pipeline better than per-row branches
     ptx::mbar_wait(&mbar, phase);
