@@ -78,7 +78,8 @@ int misa_pool_append(const void* keys, int64_t n_keys_before, int head_dim, int 
  * ReLU(q_tj . partial-block mean) when n_t % B != 0.  Work list: item i covers the 128
  * flattened (t, j) rows of tile it_tile[i] against block chunk it_chunk[i] with
  * it_ncols[i] (multiple of 16, <= 128; 0 = partial-block term only) pooled columns;
- * items are grouped by chunk.  Rows whose chunk c has no item are not written. */
+ * items are grouped by chunk.  Rows whose chunk c has no item are not written.
+ * n_heads_pad: a power of two in [8, 128]. */
 int misa_route_scores(const void* queries, int64_t n_rows, int n_heads_pad, int head_dim, const void* pooled_planes,
                       int64_t planes_rows, const float* prefix_sums, const int32_t* prefix_len, int block_size,
                       const int32_t* it_tile, const int32_t* it_chunk, const int32_t* it_ncols, int n_items,

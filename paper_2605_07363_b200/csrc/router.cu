@@ -393,8 +393,8 @@ extern "C" int misa_route_scores(const void* queries, int64_t n_rows, int n_head
                                  void* stream) {
   MISA_REQUIRE(queries && pooled_planes && prefix_sums && prefix_len && partial, "null pointer");
   MISA_REQUIRE(head_dim == 64 || head_dim == 128, "head_dim must be padded to 64 or 128");
-  MISA_REQUIRE(n_heads_pad >= 1 && n_heads_pad <= 128 && (n_heads_pad & (n_heads_pad - 1)) == 0,
-               "n_heads_pad must be a power of two <= 128");
+  MISA_REQUIRE(n_heads_pad >= 8 && n_heads_pad <= 128 && (n_heads_pad & (n_heads_pad - 1)) == 0,
+               "n_heads_pad must be a power of two in [8, 128] (<= 16 query rows per 128-row tile)");
   MISA_REQUIRE(block_size >= 1 && n_rows >= 1, "bad sizes");
   MISA_REQUIRE(n_items == 0 || (it_tile && it_chunk && it_ncols), "null work list");
   if (n_items == 0) return MISA_OK;
