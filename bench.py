@@ -192,9 +192,16 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # dev check of the N>1 path on a 1-GPU box: every rank on cuda:0, gloo transport
+    shared = os.environ.get("MISA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -327,8 +334,8 @@ def run_ours(a):
             Kd.copy_(Kh, non_blocking=True)
             Qd.copy_(Qh, non_blocking=True)
             Wd.copy_(Wh, non_blocking=True)
-            r = est_engine.run(Kd, Qd, Wd)
-            out_h.copy_(r.topk, non_blocking=True)
+            r = est_engine.run(Kd, Qd, Wd)  # this rank's row slice of the global top-k
+            out_h[: r.shape[0]].copy_(r, non_blocking=True)
 
         e2e_ms = max_over_ranks(_time_steps(step_e2e, a.steps, max(1, a.warmup), barrier))
         h2d = K.numel() * 2 + Q.numel() * 2 + W.numel() * 4
