@@ -251,12 +251,11 @@ __global__ void __launch_bounds__(192, 1)
         for (int c = 0; c < D / 8; ++c) {
           const uint4 u = *reinterpret_cast<const uint4*>(qa + ptx::sw128_offset(lrow, c * 8, C::A_ATOM));
           const float4 p0 = pv[2 * c], p1 = pv[2 * c + 1];
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-          float2 f;
-          f = __bfloat1622float2(h[0]); d0 = fmaf(f.x, p0.x, d0); d0 = fmaf(f.y, p0.y, d0);
-          f = __bfloat1622float2(h[1]); d1 = fmaf(f.x, p0.z, d1); d1 = fmaf(f.y, p0.w, d1);
-          f = __bfloat1622float2(h[2]); d2 = fmaf(f.x, p1.x, d2); d2 = fmaf(f.y, p1.y, d2);
-          f = __bfloat1622float2(h[3]); d3 = fmaf(f.x, p1.z, d3); d3 = fmaf(f.y, p1.w, d3);
+          // bf16 -> f32 is exact bit placement: low half << 16, high half masked
+          d0 = fmaf(__uint_as_float(u.x << 16), p0.x, d0); d0 = fmaf(__uint_as_float(u.x & 0xffff0000u), p0.y, d0);
+          d1 = fmaf(__uint_as_float(u.y << 16), p0.z, d1); d1 = fmaf(__uint_as_float(u.y & 0xffff0000u), p0.w, d1);
+          d2 = fmaf(__uint_as_float(u.z << 16), p1.x, d2); d2 = fmaf(__uint_as_float(u.z & 0xffff0000u), p1.y, d2);
+          d3 = fmaf(__uint_as_float(u.w << 16), p1.z, d3); d3 = fmaf(__uint_as_float(u.w & 0xffff0000u), p1.w, d3);
         }
         const float dot = (d0 + d1) + (d2 + d3);
         sum = fmaxf(dot / (float)rem, 0.f);
@@ -278,17 +277,30 @@ __global__ void __launch_bounds__(192, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);  // accumulator drained: the next tile's MMA may start
         if (++acc == 2) { acc = 0; aph ^= 1; }
-        float ps[4] = {0.f, 0.f, 0.f, 0.f};
+        // column i -> partial sum i % 4, kept as two packed pairs (FADD2); a slice wholly
+        // inside the row's valid columns skips the per-column guard
+        float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+        auto relu = [&](int col) { return fmaxf(__uint_as_float(r[col]), 0.f); };
 #pragma unroll
         for (int c = 0; c < 128; c += 32)
           if (c < ncols) {
+            if (c + 32 <= lim) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c + i < lim) ps[i & 3] += fmaxf(__uint_as_float(r[c + i]), 0.f);
+              for (int i = 0; i < 32; i += 4) {
+                pa = __fadd2_rn(pa, make_float2(relu(c + i), relu(c + i + 1)));
+                pb = __fadd2_rn(pb, make_float2(relu(c + i + 2), relu(c + i + 3)));
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                const int e = c + i;
+                pa = __fadd2_rn(pa, make_float2(e < lim ? relu(e) : 0.f, e + 1 < lim ? relu(e + 1) : 0.f));
+                pb = __fadd2_rn(pb, make_float2(e + 2 < lim ? relu(e + 2) : 0.f, e + 3 < lim ? relu(e + 3) : 0.f));
+              }
+            }
           }
-        // summation order: blocks in column order, then the partial block (as before: the
-        // partial block was added last)
-        const float full = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        // summation order: blocks in column order, then the partial block last
+        const float full = (pa.x + pa.y) + (pb.x + pb.y);
         sum = full + sum;
       }
       ptx::mbar_arrive(&empty_a[s]);
