@@ -1658,6 +1658,25 @@ __global__ void __launch_bounds__(kGlbThreads) dense_global_kernel(const float* 
 // under/overflow are flagged for the single-CTA exact path.
 constexpr int kSegThreads = 256, kSegPer = 16, kSeg = kSegThreads * kSegPer;
 
+// The thread's kSegPer consecutive scores of a segment (index order within the thread):
+// four 16-byte loads when the row is aligned and the slice is inside the row.
+__device__ __forceinline__ void seg_load(const float* __restrict__ row, int i0, int n, bool vec, float (&x)[kSegPer]) {
+  if (vec && i0 + kSegPer <= n) {
+    const float4* r4 = reinterpret_cast<const float4*>(row + i0);
+#pragma unroll
+    for (int v = 0; v < kSegPer / 4; ++v) {
+      const float4 f = __ldg(r4 + v);
+      x[4 * v] = f.x;
+      x[4 * v + 1] = f.y;
+      x[4 * v + 2] = f.z;
+      x[4 * v + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kSegPer; ++e) x[e] = i0 + e < n ? row[i0 + e] : -INFINITY;
+  }
+}
+
 __global__ void __launch_bounds__(kSegThreads) seg_count_kernel(const float* __restrict__ s, int64_t ld,
                                                                const int32_t* __restrict__ row_len,
                                                                const float* __restrict__ tau,
@@ -1667,9 +1686,9 @@ __global__ void __launch_bounds__(kSegThreads) seg_count_kernel(const float* __r
   const float tv = tau[t];
   const float* row = s + (int64_t)t * ld;
   const int i0 = sg * kSeg + threadIdx.x * kSegPer;
+  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(s) & 15) == 0);
   float x[kSegPer];
-#pragma unroll
-  for (int e = 0; e < kSegPer; ++e) x[e] = i0 + e < n ? row[i0 + e] : -INFINITY;
+  seg_load(row, i0, n, vec, x);
   int c = 0;
 #pragma unroll
   for (int e = 0; e < kSegPer; ++e) c += (i0 + e < n) && x[e] >= tv;
@@ -1711,9 +1730,9 @@ __global__ void __launch_bounds__(kSegThreads) seg_compact_kernel(const float* _
   __syncthreads();
   const int base = sbase;
   const int i0 = sg * kSeg + threadIdx.x * kSegPer;
+  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(s) & 15) == 0);
   float x[kSegPer];
-#pragma unroll
-  for (int e = 0; e < kSegPer; ++e) x[e] = i0 + e < n ? row[i0 + e] : -INFINITY;
+  seg_load(row, i0, n, vec, x);
   uint32_t selm = 0;
 #pragma unroll
   for (int e = 0; e < kSegPer; ++e) selm |= ((i0 + e < n) && x[e] >= tv ? 1u : 0u) << e;

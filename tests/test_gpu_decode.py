@@ -72,20 +72,21 @@ def test_pooled_key_cache_decode_equals_full_recompute():
     assert torch.equal(a.heads, b.heads) and torch.equal(a.topk, b.topk)
 
 
-@pytest.mark.parametrize("quantize", [False, True])
-def test_dense_long_selector_matches_sort(quantize):
+@pytest.mark.parametrize("quantize,T,L", [(False, 6, 50000), (True, 6, 50000), (False, 40, 600000)])
+def test_dense_long_selector_matches_sort(quantize, T, L):
     """misa_select_dense_long on long rows (incl. heavy ties -> on-device exact re-selection)
-    equals a (score desc, index asc) sort."""
+    equals a (score desc, index asc) sort.  The 40 x 600K case runs ~6000 look-back segments."""
     from paper_2605_07363_b200 import _lib
     torch.manual_seed(11)
-    T, L, k = 6, 50000, 700
+    k = 700
     s = torch.randn(T, L, device="cuda")
     if quantize:
         s = (s * 2).round() / 2  # few distinct values: ties at the cut, candidate overflow
-    n = torch.tensor([L, L - 1, 4000, 701, 700, 30000], dtype=torch.int32, device="cuda")
+    n = torch.tensor(([L, L - 1, 4000, 701, 700, 30000] * T)[:T], dtype=torch.int32, device="cuda")
+    n[6:] = torch.randint(1, L + 1, (max(T - 6, 0),), dtype=torch.int32)
     cap = 2048
     n_seg = -(-L // 4096)
-    bufs = dict(tau=torch.empty(T, device="cuda"), seg=torch.empty(T, n_seg, dtype=torch.int32, device="cuda"),
+    bufs = dict(tau=torch.empty(T, device="cuda"), seg=torch.empty(T * n_seg + 1, dtype=torch.int32, device="cuda"),
                 cs=torch.empty(T, cap, device="cuda"), ci=torch.empty(T, cap, dtype=torch.int32, device="cuda"),
                 cc=torch.empty(T, dtype=torch.int32, device="cuda"))
     out = torch.empty(T, k, dtype=torch.int32, device="cuda")
@@ -97,7 +98,7 @@ def test_dense_long_selector_matches_sort(quantize):
     sc = s.cpu().numpy()
     for r in range(T):
         m = int(n[r])
-        order = np.lexsort((np.arange(m), -sc[r, :m]))[: min(k, m)]
+        order = np.argsort(-sc[r, :m], kind="stable")[: min(k, m)]  # ties -> smaller index
         exp = np.sort(order)
         got = out[r].cpu().numpy()
         assert got[: len(exp)].tolist() == exp.tolist(), r
