@@ -2021,6 +2021,9 @@ extern "C" int misa_merge_topk(const float* part_scores, const int32_t* part_idx
 static int misa_select_dense_clamped(const float* cs, int64_t ld, const int32_t* ci, int64_t ci_ld,
                                      const int32_t* cnt, int64_t n_rows, int k, int32_t* topk, int64_t topk_ld,
                                      float* topk_scores, cudaStream_t st) {
+  // few rows (decode): twice the threads per row halves each row's latency
+  if (n_rows * 2 <= sm_count() && ld <= 512 * 16)
+    return DenseL<512, 16>::go(st, cs, ld, ci, ci_ld, cnt, nullptr, n_rows, k, topk, topk_ld, topk_scores);
   const int rc = dispatch_capacity<DenseL>(ld, st, cs, ld, ci, ci_ld, cnt, nullptr, n_rows, k, topk, topk_ld,
                                            topk_scores);
   MISA_REQUIRE(rc != -100, "candidate capacity %lld exceeds the register selector", (long long)ld);
@@ -2039,7 +2042,13 @@ extern "C" int misa_select_dense_long(const float* scores, int64_t ld, const int
   const int64_t m = (max_len + stride - 1) / stride;
   // tau: ~2k of the row's keys pass; rows with n <= cap keep every key
   MISA_REQUIRE(beta >= 1.0f, "beta must be >= 1");
-  int rc = dispatch_capacity<ThresholdStepL>(m, st, scores, ld, row_len, n_rows, stride, k, beta, (int64_t)cap, tau);
+  const bool few = n_rows * 2 <= sm_count();  // decode: more threads per row, lower latency
+  int rc = (few && m <= 512 * 16)
+               ? ThresholdStepL<512, 16>::go(st, scores, ld, row_len, n_rows, stride, k, beta, (int64_t)cap, tau)
+           : (few && m <= 1024 * 16)
+               ? ThresholdStepL<1024, 16>::go(st, scores, ld, row_len, n_rows, stride, k, beta, (int64_t)cap, tau)
+               : dispatch_capacity<ThresholdStepL>(m, st, scores, ld, row_len, n_rows, stride, k, beta, (int64_t)cap,
+                                                   tau);
   MISA_REQUIRE(rc != -100, "long-row sample exceeds the register selector (max_len %lld)", (long long)max_len);
   if (rc) return rc;
   const int n_seg = (int)((max_len + kSeg - 1) / kSeg);
