@@ -353,7 +353,18 @@ __global__ void route_select_kernel(const float* __restrict__ partial, int n_chu
         e = sqrtf(ss);
       } else {
         float s = 0.f;
-        for (int c = 0; c < nch && c < n_chunks; ++c) s += partial[((int64_t)c * T + t) * Hp + j];
+        const int nc = nch < n_chunks ? nch : n_chunks;
+        const float* pp = partial + (int64_t)t * Hp + j;
+        const int64_t cs = (int64_t)T * Hp;
+        int c = 0;
+        for (; c + 4 <= nc; c += 4) {  // four loads in flight, summed in chunk order
+          const float a0 = pp[c * cs], a1 = pp[(c + 1) * cs], a2 = pp[(c + 2) * cs], a3 = pp[(c + 3) * cs];
+          s += a0;
+          s += a1;
+          s += a2;
+          s += a3;
+        }
+        for (; c < nc; ++c) s += pp[c * cs];
         e = M > 0 ? fabsf(wj) * s / (float)M : 0.f;
       }
       v[r] = e != e ? -INFINITY : e;  // NaN never wins (and never breaks the argmax)
@@ -381,7 +392,8 @@ __global__ void route_select_kernel(const float* __restrict__ partial, int n_chu
         bj = oj;
       }
     }
-    if (bj != 0x7fffffff && (bj & 31) == lane) taken[(bj >> 5) & 3] = true;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) taken[r] |= bj == lane + 32 * r;  // static indices: taken stays in registers
   }
   int base = 0;
 #pragma unroll
