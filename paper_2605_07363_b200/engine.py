@@ -281,7 +281,7 @@ class IndexerEngine:
             stride, beta = self.stride, (self.beta or 2.0)
         else:
             stride, beta = max(1, self.stride // 2), (self.beta or 1.3)
-        stride = max(stride, -(-L // 16384))  # the threshold selector holds <= 16384 samples per row
+        stride = max(stride, -(-L // 16384))  # <= 16384 samples per row bounds the (T, L/stride) sample buffer
         cap = int(math.ceil(1.5 * beta * k / 4 / 32)) * 32
         # round up to a capacity the merge-free selector (select.cu topk5) is compiled for
         for c in V5_CAPS:
