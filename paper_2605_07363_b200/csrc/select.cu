@@ -1108,7 +1108,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uin
 // needs no merge: the scorer's quadrant q holds exactly the 32-key chunks c = idx/32
 // with c % 4 == q, so all selected elements of a chunk are contiguous in one list and
 //   pos = #selected in chunks < c (block scan of a chunk histogram) + rank within c.
-template <int NT, int EPT>
+template <int NT, int EPT, bool WS>  // WS: selected scores are returned too (topk_scores)
 __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_kernel(const uint64_t* __restrict__ cand,
                                                       const int32_t* __restrict__ cand_count, int cap,
                                                       const int32_t* __restrict__ prefix_len, int n_rows, int k,
@@ -1125,7 +1125,7 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
   uint32_t* G0 = H + n_chunks;                                          // first compacted rank of a chunk
   int32_t* cidx = reinterpret_cast<int32_t*>(G0 + n_chunks);            // compacted indices
   float* csc = reinterpret_cast<float*>(cidx + k);                       // compacted scores (optional)
-  const bool want_scores = topk_scores != nullptr;
+  constexpr bool want_scores = WS;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int q = w / WPL;                       // this warp's quadrant list
   const int i0 = (w % WPL) * WE + lane;        // list position of slot 0 (slot r: i0 + 32r)
@@ -1241,7 +1241,9 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
       idx[r] = 0;
       if (r < rv) {
         const int i = i0 + 32 * r;
-        const uint2 rw = *reinterpret_cast<const uint2*>(raw + (size_t)q * cap + (i < cq ? i : 0));
+        // i < cap always (the warps tile the list capacity): slots past the count read stale
+        // words that the key mask below discards
+        const uint2 rw = *reinterpret_cast<const uint2*>(raw + (size_t)q * cap + i);
         key[r] = i < cq ? float_key(__uint_as_float(rw.x)) : 0u;
         idx[r] = static_cast<int32_t>(rw.y);
         if (i < cq) {
@@ -1931,7 +1933,7 @@ static int launch_topk5_t(cudaStream_t st, const uint64_t* cand, const int32_t* 
                           int64_t T, int k, int n_chunks, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
   const size_t bytes = (size_t)kQuadrants * cap * 8 + (size_t)n_chunks * 8 + (size_t)k * (ts ? 8 : 4);
   if (bytes > 200 * 1024) return -100;
-  auto kern = topk5_kernel<NT, EPT>;
+  auto kern = ts ? topk5_kernel<NT, EPT, true> : topk5_kernel<NT, EPT, false>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   int per_sm = 0;
   MISA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes));
