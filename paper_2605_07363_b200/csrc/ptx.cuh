@@ -271,8 +271,10 @@ __device__ __forceinline__ uint32_t sw128_offset(uint32_t r, uint32_t k, uint32_
 // Monotone map float -> u32 (larger float -> larger key); -0.0 == +0.0 as in the
 // reference's argsort(-values) (dsa.py:74).
 __device__ __forceinline__ uint32_t float_key(float f) {
-  uint32_t u = __float_as_uint(f == 0.0f ? 0.0f : f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  // f + 0 turns -0 into +0 (IEEE round-to-nearest); then negative -> ~u, positive -> u | sign
+  // as one xor with (u >> 31 arithmetic) | sign: three instructions
+  const uint32_t u = __float_as_uint(__fadd_rn(f, 0.0f));
+  return u ^ (static_cast<uint32_t>(static_cast<int32_t>(u) >> 31) | 0x80000000u);
 }
 __device__ __forceinline__ float key_float(uint32_t k) {
   uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
