@@ -1378,7 +1378,7 @@ extern "C" int misa_debug_sel_trace(unsigned long long* host) {
 #endif
 
 // ------------------------------------------------------- dense rows ----
-template <int NT, int EPT>
+template <int NT, int EPT, bool HI, bool WS>  // HI: explicit indices (idx), WS: scores returned
 __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(const float* __restrict__ s, int64_t ld,
                                                        const int32_t* __restrict__ idx, int64_t idx_ld,
                                                        const int32_t* __restrict__ row_len,
@@ -1390,9 +1390,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
   const int rr = rows ? rows[blockIdx.x] : blockIdx.x;
   const int n = min(row_len[rr], (int)ld);  // candidate counts may exceed the staged capacity
   const float* row = s + (int64_t)rr * ld;
-  const int32_t* irow = idx ? idx + (int64_t)rr * idx_ld : nullptr;
+  const int32_t* irow = HI ? idx + (int64_t)rr * idx_ld : nullptr;
   int32_t* out = topk + (int64_t)rr * topk_ld;
-  float* outs = topk_scores ? topk_scores + (int64_t)rr * topk_ld : nullptr;
+  float* outs = WS ? topk_scores + (int64_t)rr * topk_ld : nullptr;
   const int kk = n < k ? n : k;
   if (kk <= 0) {
     for (int i = threadIdx.x; i < k; i += NT) {
@@ -1417,7 +1417,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
       const int e = v3_elem<NT, E>(r);
       const int ec = e < n ? e : 0;
       x[r] = row[ec];
-      ix[r] = irow ? irow[ec] : e;
+      ix[r] = HI ? irow[ec] : e;
     }
 #pragma unroll
     for (int r = 0; r < E; ++r) {
@@ -1908,9 +1908,10 @@ struct DenseL {
                 const int32_t* row_len, const int32_t* rows, int64_t n_rows, int k, int32_t* topk, int64_t tld,
                 float* ts) {
     const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 16;
-    MISA_CUDA_TRY(
-        cudaFuncSetAttribute(dense_reg_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    dense_reg_kernel<NT, EPT><<<(unsigned)n_rows, NT, bytes, st>>>(s, ld, idx, idx_ld, row_len, rows, k, topk, tld, ts);
+    auto kern = idx ? (ts ? dense_reg_kernel<NT, EPT, true, true> : dense_reg_kernel<NT, EPT, true, false>)
+                    : (ts ? dense_reg_kernel<NT, EPT, false, true> : dense_reg_kernel<NT, EPT, false, false>);
+    MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    kern<<<(unsigned)n_rows, NT, bytes, st>>>(s, ld, idx, idx_ld, row_len, rows, k, topk, tld, ts);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
   }
