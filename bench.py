@@ -303,13 +303,14 @@ def run_ours(a):
             del Ks, Qs, Ws, xs, em, ed
 
     hier_ms = None
+    res_h = None
     hstages = {}
     if not a.no_hier and world == 1:
         eng_h = IndexerEngine("misa_hier", budget_k=a.k, active_heads_h=a.h, block_size=a.B,
                               candidate_kprime=a.kprime)
         hier_ms = _time_steps(lambda: eng_h.run_prepared(x), a.steps, a.warmup, barrier)
         eng_h.stage_events = []
-        eng_h.run_prepared(x)
+        res_h = eng_h.run_prepared(x)
         torch.cuda.synchronize()
         ev = eng_h.stage_events
         hstages = {}
@@ -329,7 +330,7 @@ def run_ours(a):
 
         def step_e2e():
             if world == 1:  # public API on pinned host tensors: copy-overlapped row-chunk pipeline
-                est.select_batch(Kh, Qh, Wh)
+                est.select_batch(Kh, Qh, Wh, out=out_h)  # the caller's pinned result buffer
                 return
             Kd.copy_(Kh, non_blocking=True)
             Qd.copy_(Qh, non_blocking=True)
@@ -363,24 +364,32 @@ def run_ours(a):
             dist.destroy_process_group()
         return
 
-    # --- recall vs the CPU reference algorithm on sampled rows (oracle, fast32, same bf16 inputs)
+    # --- recall vs the CPU reference algorithm on sampled rows (oracle, fast32, same bf16 inputs),
+    # for every method timed here: the reference's selection of row t on IndexerWorkload(K[:t+1], Q[t], W[t])
     from oracle import misa_oracle as O
-    rows = sorted(set(r for r in [2048, 8192, T // 4, T // 2, 3 * T // 4, T - 1] if r < T))
+    rows = sorted(set(r for r in [2048, 8191, 8192, 8193, T // 4, T // 2, 3 * T // 4, T - 1] if r < T))
     Kn = K.double().cpu().numpy()
-    hit = tot = 0
+    hits = {m: [0, 0] for m in ("dsa", "misa", "misa_hier") if m != "misa_hier" or res_h is not None}
     iou = []
     for t in rows:
         n = t + 1
         qs, ws = Q[t].double().cpu().numpy(), W[t].double().cpu().numpy()
-        ref = O.misa_select(Kn[:n], qs, ws, a.k, a.h, a.B, precision="fast32")["selection"]
-        got = res_m.topk[t].cpu().numpy()
-        got = set(got[got >= 0].tolist())
-        hit += len(got & set(ref.tolist()))
-        tot += len(ref)
-        gd = res_d.topk[t].cpu().numpy()
-        gd = set(gd[gd >= 0].tolist())
-        iou.append(len(got & gd) / len(got | gd))
-    recall = hit / tot
+        got = {"dsa": res_d.topk[t], "misa": res_m.topk[t]}
+        if res_h is not None:
+            got["misa_hier"] = res_h.topk[t]
+        got = {m: set(v[v >= 0].tolist()) for m, v in ((m, g.cpu().numpy()) for m, g in got.items())}
+        for m in hits:
+            if m == "dsa":
+                ref = O.dsa_select(Kn[:n], qs, ws, a.k, "fast32")["selection"]
+            elif m == "misa":
+                ref = O.misa_select(Kn[:n], qs, ws, a.k, a.h, a.B, precision="fast32")["selection"]
+            else:
+                ref = O.misa_hier_select(Kn[:n], qs, ws, a.k, a.h, a.B, a.kprime, precision="fast32")["selection"]
+            hits[m][0] += len(got[m] & set(ref.tolist()))
+            hits[m][1] += len(ref)
+        iou.append(len(got["misa"] & got["dsa"]) / len(got["misa"] | got["dsa"]))
+    recall_by = {m: round(hv[0] / hv[1], 6) for m, hv in hits.items()}
+    recall = recall_by["misa"]
 
     # --- roofline of the dominant kernel (MISA token scoring, tcgen05)
     P = L * (L + 1) // 2                       # causal scored pairs per layer
@@ -440,7 +449,7 @@ def run_ours(a):
                    "k": a.k, "parallelism": f"key-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (queries 2 GiB); no explicit flush"},
         "dsa_ms_per_layer": round(dsa_ms, 3), "speedup_vs_dsa": round(dsa_ms / misa_ms, 3),
-        "topk_recall_vs_cpu_reference": round(recall, 6), "recall_rows": rows,
+        "topk_recall_vs_cpu_reference": round(recall, 6), "topk_recall_by_method": recall_by, "recall_rows": rows,
         "misa_iou_vs_dsa_random_data": round(float(np.mean(iou)), 4),
         "scores_per_s": P / (misa_ms * 1e-3), "layer_tensor_frac": round(layer_frac, 4),
         "misa_stages_ms": {k: round(v, 4) for k, v in stages.items()},

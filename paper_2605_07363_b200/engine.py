@@ -411,11 +411,14 @@ class IndexerEngine:
         """K5 + dense select within candidates (MISA-dagger fine stage)."""
         dev = x.keys.device
         kp = cand.shape[1]
-        ncand_host = np.minimum(x.prefix_host, kp)
         ckey = x.causal_key or x.prefix_host.tobytes()
-        ncand, rows = self._dev_list(("refine", ckey, kp),
-                                     lambda: (ncand_host.astype(np.int32),
-                                              np.argsort(-ncand_host, kind="stable").astype(np.int32)), dev)
+        # the candidate count of row t is min(n_t, k'), taken from the device prefix lengths:
+        # under a CUDA graph (DecodeGraph) the host lengths are the bucket's, not the cache's
+        ncand = self._buf("refine_ncand", (x.T,), torch.int32, dev)
+        torch.clamp_max(x.prefix, kp, out=ncand)
+        (rows,) = self._dev_list(("refine_rows", ckey, kp),  # schedule only: longest rows first
+                                 lambda: (np.argsort(-np.minimum(x.prefix_host, kp), kind="stable").astype(np.int32),),
+                                 dev)
         rs = self._buf("refine_scores", (x.T, kp), torch.float32, dev)
         stream = self._stream()
         self._mark("refine")
@@ -565,11 +568,10 @@ class IndexerEngine:
                             dtype=np.int64).reshape(-1)
         dev = torch.device("cuda")
         k = self.k
-        if out is None:
-            out = self._ws.get("host_out")
-            if out is None or tuple(out.shape) != (T, k):
-                out = torch.empty(T, k, dtype=torch.int32).pin_memory()
-                self._ws["host_out"] = out
+        if out is None:  # a fresh result per call (the caller owns it); pass `out` to reuse a pinned buffer
+            out = torch.empty(T, k, dtype=torch.int32, pin_memory=True)
+        elif tuple(out.shape) != (T, k) or out.dtype != torch.int32 or out.is_cuda:
+            raise ValueError(f"out must be a host (T={T}, k={k}) int32 tensor")
         # chunk boundaries with ~equal work (sum of prefix lengths)
         cw = np.cumsum(pl)
         cuts = [0] + [int(np.searchsorted(cw, cw[-1] * (c + 1) / chunks)) + 1 for c in range(chunks - 1)] + [T]
@@ -626,6 +628,7 @@ class IndexerEngine:
                 ev_out[c].record(s_out)
         for e in ev_out:
             comp.wait_event(e)
+        ev_out[-1].synchronize()  # the D2H copies are stream-ordered on s_out: the last one covers all
         if self.check_overflow:
             bad = torch.nonzero(flags_all).flatten().cpu().numpy()
             if bad.size:  # exact re-run of just those rows (the device path's own fallback)
@@ -716,6 +719,10 @@ class DecodeGraph:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
             self.result = eng.decode_prepared(x, cache=c, out=self.out)
+        # the graph holds raw device pointers into the engine's workspace and cached work
+        # lists: keep those tensors alive for the graph's lifetime, even if a later eager call
+        # on the same engine swaps in larger buffers or clears the work-list cache
+        self._keep = (list(eng._ws.values()), list(eng._lists.values()))
         self.graph, self.Lb = g, Lb
 
     def step(self, queries, weights) -> IndexerOutput:

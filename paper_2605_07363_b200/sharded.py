@@ -132,13 +132,15 @@ class ShardedIndexer:
         self.last_fallback_rows = 0
 
     def _local_keys(self, x: PreparedInputs) -> torch.Tensor:
-        key = (x.keys.data_ptr(), x.L, x.D)
-        kl = self._cache.get("keys")
-        if kl is None or kl[0] != key:
+        """This shard's keys, gathered on every call: a key buffer may be rewritten in place
+        between layers (or be a temporary the allocator hands back at the same address), so
+        nothing keyed on its address may be cached.  Only the index list is cached (it
+        depends on L alone); the gather is one pass over L*D*2 bytes."""
+        idx = self._cache.get(("idx", x.L, x.keys.device))
+        if idx is None:
             idx = torch.from_numpy(self.layout.local_keys(x.L)).to(x.keys.device)
-            kl = (key, x.keys.index_select(0, idx).contiguous())
-            self._cache["keys"] = kl
-        return kl[1]
+            self._cache = {("idx", x.L, x.keys.device): idx}
+        return x.keys.index_select(0, idx)
 
     def run(self, keys, queries, weights, prefix_len=None, *, gather: bool = False):
         x = prepare_inputs(keys, queries, weights, prefix_len)

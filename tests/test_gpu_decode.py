@@ -131,6 +131,55 @@ def test_decode_graph_replay_matches_eager(method):
             assert torch.equal(got.heads, ref.heads)
 
 
+def test_decode_graph_misa_hier_short_cache_signed_gates():
+    """MISA-dagger under DecodeGraph with a cache shorter than k' and not a bucket multiple:
+    the candidate count comes from the device prefix (not the bucket length), so padded
+    candidate slots never compete in the re-rank, even with signed gates (negative scores)."""
+    from paper_2605_07363_b200 import DecodeGraph, IndexerEngine
+    from paper_2605_07363_b200.pooling import PooledKeyCache
+    T, k, B, kp = 3, 256, 512, 4096
+    g = torch.Generator(device="cuda").manual_seed(41)
+    K = torch.randn(3000, 128, device="cuda", generator=g).bfloat16()
+    Q = torch.randn(3 * T, 16, 128, device="cuda", generator=g).bfloat16()
+    W = torch.randn(3 * T, 16, device="cuda", generator=g)  # signed gates: most scores negative
+    cache = PooledKeyCache(128, B, capacity=8192)
+    cache.append(K[:1500])
+    kw = dict(budget_k=k, active_heads_h=4, block_size=B, candidate_kprime=kp)
+    dg = DecodeGraph(IndexerEngine("misa_hier", **kw), cache, T, 16, bucket=1024)
+    for step, L in enumerate((1500, 2100, 3000)):
+        if cache.length < L:
+            cache.append(K[cache.length:L])
+        q, w = Q[step * T:(step + 1) * T], W[step * T:(step + 1) * T]
+        got = dg.step(q, w)
+        ref = IndexerEngine("misa_hier", **kw).decode(queries=q, weights=w, cache=cache)
+        torch.cuda.synchronize()
+        assert torch.equal(got.topk, ref.topk), L
+        assert (got.topk >= 0).all() and (got.topk < L).all()
+
+
+def test_decode_graph_survives_engine_reuse():
+    """Eager calls with larger shapes on the graph's engine (new workspace, work-list cache
+    churn) must not invalidate the captured graph: it keeps its buffers alive."""
+    from paper_2605_07363_b200 import DecodeGraph, IndexerEngine
+    from paper_2605_07363_b200.pooling import PooledKeyCache
+    T, k, B = 4, 256, 1024
+    K, Q, W = _inputs(12000, 80, seed=43)
+    cache = PooledKeyCache(128, B, capacity=16384)
+    cache.append(K[:9000])
+    eng = IndexerEngine("misa", budget_k=k, active_heads_h=8, block_size=B)
+    dg = DecodeGraph(eng, cache, T, 64)
+    first = dg.step(Q[:T], W[:T]).topk.clone()
+    for n in range(70):  # > 64 distinct work lists: the engine clears its cache
+        eng.decode(K[:12000], Q[:8], W[:8], prefix_len=np.full(8, 3000 + 100 * n))
+    eng.run(K, Q[:80], W[:80], prefix_len=np.arange(11921, 12001))  # larger workspace
+    torch.cuda.synchronize()
+    again = dg.step(Q[:T], W[:T]).topk
+    ref = IndexerEngine("misa", budget_k=k, active_heads_h=8, block_size=B).decode(queries=Q[:T], weights=W[:T],
+                                                                                   cache=cache)
+    torch.cuda.synchronize()
+    assert torch.equal(again, first) and torch.equal(again, ref.topk)
+
+
 @pytest.mark.parametrize("method,G", [("misa", 2), ("misa", 8), ("dsa", 4)])
 def test_virtual_key_shards_decode_merge_to_single_gpu(method, G):
     """G key shards on one GPU: per-shard decode top-k with scores -> global index map ->

@@ -23,8 +23,15 @@ def worker(rank, world, port, q):
     for m in ("misa", "dsa", "misa_hier"):
         kw = dict(budget_k=k, active_heads_h=8, block_size=B, candidate_kprime=2048)
         ref = IndexerEngine(m, **kw).run(K, Q, W).topk
-        got = ShardedIndexer(m, world=world, rank=rank, **kw).run(K, Q, W, gather=True)
+        sh = ShardedIndexer(m, world=world, rank=rank, **kw)
+        Kbuf = K.clone()
+        got = sh.run(Kbuf, Q, W, gather=True)
         ok[m + "_prefill"] = bool(torch.equal(got, ref))
+        # the same key buffer rewritten in place (next layer) through the same sharded indexer
+        Kbuf.copy_(torch.randn(L, d, device="cuda", generator=g).bfloat16())
+        ref2 = IndexerEngine(m, **kw).run(Kbuf, Q, W).topk
+        ok[m + "_prefill_rewritten_keys"] = bool(torch.equal(sh.run(Kbuf, Q, W, gather=True), ref2))
+        del Kbuf
         Qd, Wd = Q[-8:].contiguous(), W[-8:].contiguous()
         refd = IndexerEngine(m, **kw).decode(K, Qd, Wd).topk
         gotd = ShardedIndexer(m, world=world, rank=rank, **kw).decode(K, Qd, Wd)
