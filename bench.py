@@ -62,6 +62,7 @@ def _args():
     p.add_argument("--no-needle", action="store_true", help="skip the needle-retrieval recall leg")
     p.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
     p.add_argument("--no-sweep", action="store_true", help="skip the C2 / C3 prefill configs")
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 1M-key causal prefill leg")
     return p.parse_args()
 
 
@@ -182,6 +183,48 @@ def _time_steps(fn, steps, warmup, barrier):
     torch.cuda.synchronize()
     barrier()
     return e0.elapsed_time(e1) / steps
+
+
+def c5_prefill_leg(a, tc_burst, barrier):
+    """C5 on one GPU: causal prefill at L = T = 2^20 (row passes bounded by the workspace),
+    MISA and the dense DSA kernel, plus sampled-row recall against the CPU oracle."""
+    import torch
+    from paper_2605_07363_b200 import IndexerEngine, prepare_inputs
+    from oracle import misa_oracle as O
+    L5 = T5 = 1 << 20
+    g5 = torch.Generator(device="cuda").manual_seed(5)
+    K5 = torch.randn(L5, a.d, device="cuda", generator=g5).bfloat16()
+    Q5 = torch.randn(T5, a.H, a.d, device="cuda", generator=g5).bfloat16()
+    W5 = torch.softmax(torch.randn(T5, a.H, device="cuda", generator=g5), -1).float()
+    x5 = prepare_inputs(K5, Q5, W5)
+    em = IndexerEngine("misa", budget_k=a.k, active_heads_h=a.h, block_size=a.B)
+    out = torch.empty(T5, a.k, dtype=torch.int32, device="cuda")
+    ms_m = _time_steps(lambda: em.run_prepared(x5, out=out), 2, 1, barrier)
+    passes = -(-T5 // em.row_chunk(x5))
+    rows = [2048, 262144, 786432, T5 - 1]
+    sel = torch.tensor(rows, device="cuda")
+    got = out[sel].cpu().numpy()
+    del em
+    torch.cuda.empty_cache()
+    ed = IndexerEngine("dsa", budget_k=a.k)
+    ms_d = _time_steps(lambda: ed.run_prepared(x5, out=out), 1, 1, barrier)
+    del ed
+    Kn = K5.double().cpu().numpy()
+    Qn, Wn = Q5[sel].double().cpu().numpy(), W5[sel].double().cpu().numpy()
+    del x5, K5, Q5, W5, out
+    torch.cuda.empty_cache()
+    hit = tot = 0
+    for i, t in enumerate(rows):
+        ref = O.misa_select(Kn[: t + 1], Qn[i], Wn[i], a.k, a.h, a.B, precision="fast32")["selection"]
+        g = got[i][got[i] >= 0]
+        hit += len(set(g.tolist()) & set(ref.tolist()))
+        tot += len(ref)
+    P5 = L5 * (L5 + 1) // 2
+    return {"workload": f"C5 causal prefill L=T={L5} H={a.H} h={a.h} d={a.d} B={a.B} k={a.k}, 1 GPU",
+            "misa_ms": round(ms_m, 2), "dsa_ms": round(ms_d, 2), "speedup_vs_dsa": round(ms_d / ms_m, 3),
+            "row_passes": passes, "misa_scores_per_s": P5 / (ms_m * 1e-3),
+            "misa_tensor_frac_burst": round(2.0 * a.h * a.d * P5 / (ms_m * 1e-3) / 1e12 / tc_burst, 4),
+            "topk_recall_vs_cpu_reference": round(hit / tot, 6), "recall_rows": rows}
 
 
 def run_ours(a):
@@ -317,6 +360,8 @@ def run_ours(a):
         for (n0, e0), (_, e1) in zip(ev, ev[1:]):
             hstages[n0] = hstages.get(n0, 0.0) + e0.elapsed_time(e1)
         eng_h.stage_events = None
+        res_h = type("R", (), {"topk": res_h.topk})()  # drop the views into the engine's workspace
+        del eng_h
 
     # --- e2e through the public API: pinned host buffers, H2D each step, D2H of the top-k
     e2e = None
@@ -434,6 +479,12 @@ def run_ours(a):
                           "eager engine.decode and CUDA-graph DecodeGraph replay, ms per step",
                   "rows": decode_numbers()}
 
+    c5 = None
+    if world == 1 and not a.no_c5:
+        del eng_m, eng_d, x
+        torch.cuda.empty_cache()
+        c5 = c5_prefill_leg(a, tc_burst, barrier)
+
     needle = None
     if world == 1 and not a.no_needle:
         sys.path.insert(0, os.path.join(REPO, "tools"))
@@ -456,7 +507,7 @@ def run_ours(a):
         "dsa_stages_ms": {k: round(v, 4) for k, v in dstages.items()},
         "fallback_rows": fallback,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
-        "decode": decode, "sharded_decode": sdec, "configs": sweep, "needle": needle,
+        "decode": decode, "sharded_decode": sdec, "configs": sweep, "c5_prefill": c5, "needle": needle,
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)

@@ -32,6 +32,7 @@
  *   misa_refine_scores    dsa.py:95-115      dsa_rescore (MISA-dagger fine stage), routing.py:144-174
  *   misa_merge_topk       (no reference counterpart: key-sharded multi-GPU merge)
  *   misa_shard_map_indices (no reference counterpart: local -> global key index of a shard)
+ *   misa_list_kth / misa_list_prune (no reference counterpart: pruned key-shard exchange)
  */
 #ifndef MISA_B200_H_
 #define MISA_B200_H_
@@ -163,15 +164,31 @@ int misa_select_dense_long(const float* scores, int64_t ld, const int32_t* row_l
 
 /* MISA-dagger fine stage: out[t*out_ld + i] = sum_j w_tj ReLU(q_tj . key[cand[t][i]]) over all
  * heads, for i < n_cand[t] (cand ascending, -1 padded), for the rows listed in rows[0..n_items)
- * (longest first).  Gathered-key tcgen05 contraction (TMA tile::gather4). */
+ * (longest first).  Gathered-key tcgen05 contraction (16-byte cp.async row gathers into the
+ * 128-B-swizzled operand layout; completion on the stage mbarrier). */
 int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const void* queries, const float* weights,
                        int n_heads, int n_heads_pad, const int32_t* cand, int64_t cand_ld, const int32_t* n_cand,
                        const int32_t* rows, int n_items, int64_t n_rows, float* out, int64_t out_ld, void* stream);
 
 /* Multi-GPU merge: n_parts local (score, index) top-k lists per row (parts[p][t][i], scores
- * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc). */
+ * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc).
+ * topk_scores (optional) receives the selected scores aligned with topk (-inf padded), so
+ * merges can be chained when n_parts * k_in exceeds one CTA's register capacity (16384). */
 int misa_merge_topk(const float* part_scores, const int32_t* part_idx, int n_parts, int64_t part_stride,
-                    int64_t n_rows, int k_in, int k, int32_t* topk, int64_t topk_ld, void* stream);
+                    int64_t n_rows, int k_in, int k, int32_t* topk, int64_t topk_ld, float* topk_scores,
+                    void* stream);
+
+/* Key-shard exchange pruning (no reference counterpart).  tau[t] = the m-th
+ * largest score of row t's list (scores[t][0..n_cols), -inf entries are padding), or -inf when
+ * the row holds fewer than m entries.  With m_g entries per shard summing to k, the global k-th
+ * score is >= min over shards of their tau: entries below it cannot be selected. */
+int misa_list_kth(const float* scores, int64_t ld, int64_t n_rows, int n_cols, int m, float* tau, void* stream);
+
+/* Order-preserving compaction of the entries with score >= tau[t] (and index >= 0) of each
+ * row into out (n_rows x cap, -1 / -inf padded); count[t] = the number kept (a row with
+ * count > cap was truncated and must be exchanged unpruned). */
+int misa_list_prune(const float* scores, const int32_t* idx, int64_t ld, int64_t n_rows, int n_cols,
+                    const float* tau, int cap, float* out_scores, int32_t* out_idx, int32_t* count, void* stream);
 
 /* Block-cyclic key sharding: in place, local key index i of shard `shard` (of n_shards,
  * blocks of `block` keys) -> global index ((i / block) * n_shards + shard) * block + i % block;

@@ -47,7 +47,9 @@ SIGNATURES: dict[str, list] = {
                                _vp, _vp],
     "misa_refine_scores": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
                            _vp],
-    "misa_merge_topk": [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _vp, _i64, _vp],
+    "misa_merge_topk": [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _vp, _i64, _vp, _vp],
+    "misa_list_kth": [_vp, _i64, _i64, _i32, _i32, _vp, _vp],
+    "misa_list_prune": [_vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     "misa_shard_map_indices": [_vp, _i64, _i32, _i32, _i32, _vp],
 }
 EXTRA = {"misa_abi_version": ([], ctypes.c_int), "misa_last_error": ([], ctypes.c_char_p),

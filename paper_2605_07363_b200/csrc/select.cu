@@ -1781,7 +1781,8 @@ __global__ void __launch_bounds__(kGlbThreads) seg_fixup_kernel(const float* __r
 template <int NT, int EPT>
 __global__ void __launch_bounds__(NT) merge_kernel(const float* __restrict__ ps, const int32_t* __restrict__ pi,
                                                    int n_parts, int64_t part_stride, int k_in, int k,
-                                                   int32_t* __restrict__ topk, int64_t topk_ld) {
+                                                   int32_t* __restrict__ topk, int64_t topk_ld,
+                                                   float* __restrict__ topk_scores) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ SelSh<NT> sh;
   const int t = blockIdx.x;
@@ -1801,13 +1802,18 @@ __global__ void __launch_bounds__(NT) merge_kernel(const float* __restrict__ ps,
   __syncthreads();
   const int N = sh.lst_off[n_parts];
   int32_t* out = topk + (int64_t)t * topk_ld;
+  float* outs = topk_scores ? topk_scores + (int64_t)t * topk_ld : nullptr;
   const int kk = N < k ? N : k;
   if (kk <= 0) {
-    for (int i = threadIdx.x; i < k; i += NT) out[i] = -1;
+    for (int i = threadIdx.x; i < k; i += NT) {
+      out[i] = -1;
+      if (outs) outs[i] = -INFINITY;
+    }
     return;
   }
   int32_t* sidx = reinterpret_cast<int32_t*>(dsm);
   int32_t* cidx = sidx + NT * EPT;
+  float* csc = reinterpret_cast<float*>(cidx + 2 * k);
   auto load = [&](auto& key, int32_t* si) {
     constexpr int E = sizeof(key) / sizeof(key[0]);
 #pragma unroll
@@ -1823,7 +1829,76 @@ __global__ void __launch_bounds__(NT) merge_kernel(const float* __restrict__ ps,
       }
     }
   };
-  v3_dispatch<NT, EPT>(N, load, n_parts, kk, sh, sidx, cidx, nullptr, out, nullptr, k);
+  v3_dispatch<NT, EPT>(N, load, n_parts, kk, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
+}
+
+// m-th largest score of each row's list (-inf entries are padding): block-wide bit search.
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) list_kth_kernel(const float* __restrict__ s, int64_t ld, int n_cols, int m,
+                                                      float* __restrict__ tau) {
+  __shared__ SelSh<NT> sh;
+  const float* row = s + (int64_t)blockIdx.x * ld;
+  uint32_t key[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = r * NT + threadIdx.x;
+    const float v = i < n_cols ? row[i] : -INFINITY;
+    key[r] = v == -INFINITY ? 0u : float_key(v);
+  }
+  int parity = 0;
+  const int nv = block_count<NT, EPT>([&](int r) { return key[r] != 0u; }, sh, parity);
+  if (nv < m) {  // block-uniform
+    if (threadIdx.x == 0) tau[blockIdx.x] = -INFINITY;
+    return;
+  }
+  int cge, cgt;
+  const uint32_t v = kth_largest<NT, EPT>([&](int r) { return key[r]; }, m, sh, parity, &cge, &cgt);
+  if (threadIdx.x == 0) tau[blockIdx.x] = key_float(v);
+}
+
+// Stable compaction of the entries >= tau (one CTA per row, NT-wide tiles in order).
+template <int NT>
+__global__ void __launch_bounds__(NT) list_prune_kernel(const float* __restrict__ s, const int32_t* __restrict__ ix,
+                                                        int64_t ld, int n_cols, const float* __restrict__ tau, int cap,
+                                                        float* __restrict__ os, int32_t* __restrict__ oi,
+                                                        int32_t* __restrict__ count) {
+  constexpr int NW = NT / 32;
+  __shared__ int wsum[NW];
+  const int t = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float th = tau[t];
+  const float* srow = s + (int64_t)t * ld;
+  const int32_t* irow = ix + (int64_t)t * ld;
+  float* orow_s = os + (int64_t)t * cap;
+  int32_t* orow_i = oi + (int64_t)t * cap;
+  int base = 0;
+  for (int c0 = 0; c0 < n_cols; c0 += NT) {
+    const int i = c0 + threadIdx.x;
+    float v = -INFINITY;
+    int32_t id = -1;
+    if (i < n_cols) {
+      v = srow[i];
+      id = irow[i];
+    }
+    const bool keep = id >= 0 && v >= th;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    const int pos = base + warps_exclusive<NW>(wsum, w) + __popc(bal & ptx::lanemask_lt());
+    if (keep && pos < cap) {
+      orow_s[pos] = v;
+      orow_i[pos] = id;
+    }
+    int tot = 0;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) tot += wsum[j];
+    base += tot;
+    __syncthreads();
+  }
+  for (int p = base + threadIdx.x; p < cap; p += NT) {
+    orow_s[p] = -INFINITY;
+    orow_i[p] = -1;
+  }
+  if (threadIdx.x == 0) count[t] = base;
 }
 
 // Block-cyclic key shard: local key i of `rank` is global key ((i / bs) * G + rank) * bs + i % bs.
@@ -1920,10 +1995,19 @@ struct DenseL {
 template <int NT, int EPT>
 struct MergeL {
   static int go(cudaStream_t st, const float* ps, const int32_t* pi, int n_parts, int64_t stride, int64_t T, int k_in,
-                int k, int32_t* topk, int64_t ld) {
-    const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 8;
+                int k, int32_t* topk, int64_t ld, float* ts) {
+    const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 16;
     MISA_CUDA_TRY(cudaFuncSetAttribute(merge_kernel<NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    merge_kernel<NT, EPT><<<(unsigned)T, NT, bytes, st>>>(ps, pi, n_parts, stride, k_in, k, topk, ld);
+    merge_kernel<NT, EPT><<<(unsigned)T, NT, bytes, st>>>(ps, pi, n_parts, stride, k_in, k, topk, ld, ts);
+    MISA_LAUNCH_CHECK();
+    return MISA_OK;
+  }
+};
+
+template <int NT, int EPT>
+struct ListKthL {
+  static int go(cudaStream_t st, const float* s, int64_t ld, int64_t T, int n_cols, int m, float* tau) {
+    list_kth_kernel<NT, EPT><<<(unsigned)T, NT, 0, st>>>(s, ld, n_cols, m, tau);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
   }
@@ -2011,14 +2095,38 @@ extern "C" int misa_select_dense(const float* scores, int64_t ld, const int32_t*
 }
 
 extern "C" int misa_merge_topk(const float* part_scores, const int32_t* part_idx, int n_parts, int64_t part_stride,
-                               int64_t n_rows, int k_in, int k, int32_t* topk, int64_t topk_ld, void* stream) {
+                               int64_t n_rows, int k_in, int k, int32_t* topk, int64_t topk_ld, float* topk_scores,
+                               void* stream) {
   MISA_REQUIRE(part_scores && part_idx && topk, "null pointer");
   MISA_REQUIRE(n_parts >= 1 && n_parts <= kMaxLists && k_in >= 1 && k >= 1 && topk_ld >= k, "bad merge arguments");
+  MISA_REQUIRE((size_t)k * 16 <= 200 * 1024, "k too large");
   if (n_rows <= 0) return MISA_OK;
   const int rc = dispatch_capacity<MergeL>((int64_t)n_parts * k_in, as_stream(stream), part_scores, part_idx,
-                                           n_parts, part_stride, n_rows, k_in, k, topk, topk_ld);
+                                           n_parts, part_stride, n_rows, k_in, k, topk, topk_ld, topk_scores);
   MISA_REQUIRE(rc != -100, "n_parts*k_in exceeds the register selector");
   return rc;
+}
+
+extern "C" int misa_list_kth(const float* scores, int64_t ld, int64_t n_rows, int n_cols, int m, float* tau,
+                             void* stream) {
+  MISA_REQUIRE(scores && tau, "null pointer");
+  MISA_REQUIRE(n_cols >= 1 && ld >= n_cols && m >= 1, "bad list_kth arguments");
+  if (n_rows <= 0) return MISA_OK;
+  const int rc = dispatch_capacity<ListKthL>(n_cols, as_stream(stream), scores, ld, n_rows, n_cols, m, tau);
+  MISA_REQUIRE(rc != -100, "list length %d exceeds the register selector", n_cols);
+  return rc;
+}
+
+extern "C" int misa_list_prune(const float* scores, const int32_t* idx, int64_t ld, int64_t n_rows, int n_cols,
+                               const float* tau, int cap, float* out_scores, int32_t* out_idx, int32_t* count,
+                               void* stream) {
+  MISA_REQUIRE(scores && idx && tau && out_scores && out_idx && count, "null pointer");
+  MISA_REQUIRE(n_cols >= 1 && ld >= n_cols && cap >= 1, "bad list_prune arguments");
+  if (n_rows <= 0) return MISA_OK;
+  list_prune_kernel<256><<<(unsigned)n_rows, 256, 0, as_stream(stream)>>>(scores, idx, ld, n_cols, tau, cap,
+                                                                          out_scores, out_idx, count);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
 }
 
 static int misa_select_dense_clamped(const float* cs, int64_t ld, const int32_t* ci, int64_t ci_ld,

@@ -92,6 +92,12 @@ class PreparedInputs:
     causal_key: tuple | None
     pages: tuple | None = None  # paged key cache: (page_table (n_pages,) int32 device, page_size)
 
+    def rows(self, a: int, b: int) -> "PreparedInputs":
+        """Rows [a, b) against the same key set (views, no copies)."""
+        ck = None if self.causal_key is None else self.causal_key + ("rows", a, b)
+        return PreparedInputs(self.keys, self.queries[a:b], self.weights[a:b], self.prefix[a:b],
+                              self.prefix_host[a:b], self.L, b - a, self.H, self.Hp, self.d, self.D, ck, self.pages)
+
 
 def prepare_inputs(keys, queries, weights, prefix_len=None, device=None, prefix_dev=None) -> PreparedInputs:
     """Move/convert/pad inputs to the kernel layouts (no copy when already conforming).
@@ -182,7 +188,7 @@ class IndexerEngine:
 
     def __init__(self, method: str = "misa", *, budget_k: int = 2048, active_heads_h: int = 8,
                  block_size: int = 1024, candidate_kprime: int = 8192, router_score: str = BLOCK_ATTENTION,
-                 sample_stride: int = 32, beta: float | None = None, workspace_bytes: int = 16 << 30,
+                 sample_stride: int = 32, beta: float | None = None, workspace_bytes: int = 32 << 30,
                  check_overflow: bool = True):
         check_choice(method, METHODS, "method")
         self.method = method
@@ -274,15 +280,18 @@ class IndexerEngine:
         """(sample stride, beta, per-quadrant candidate capacity) of the fused top-k.
 
         tau is the j-th largest score on a 1/stride key sample, j = beta*k/stride, so about
-        beta*k keys pass; its relative spread is ~1/sqrt(j).  Capacity is 1.5x the expected
-        per-quadrant count (>= 5 sigma), and rows with n <= 4*cap keep every key.
+        beta*k keys pass; its relative spread is ~1/sqrt(j).  Capacity is (1 + 5.5/sqrt(j))x
+        the expected per-quadrant count (5.5 sigma: 1.49x at j = 128, the C4 shape; 1.69x at
+        j = 64, where 1M-key rows sample every 64th key), and rows with n <= 4*cap keep
+        every key.
         """
         if k < 4096:
             stride, beta = self.stride, (self.beta or 2.0)
         else:
             stride, beta = max(1, self.stride // 2), (self.beta or 1.3)
         stride = max(stride, -(-L // 16384))  # <= 16384 samples per row bounds the (T, L/stride) sample buffer
-        cap = int(math.ceil(1.5 * beta * k / 4 / 32)) * 32
+        j = max(1.0, beta * k / stride)
+        cap = int(math.ceil((1.0 + 5.5 / math.sqrt(j)) * beta * k / 4 / 32)) * 32
         # round up to a capacity the merge-free selector (select.cu topk5) is compiled for
         for c in V5_CAPS:
             if c >= cap:
@@ -645,12 +654,55 @@ class IndexerEngine:
         x = prepare_inputs(keys, queries, weights, prefix_len)
         return self.run_prepared(x, need_importance=need_importance, out=out)
 
+    def row_chunk(self, x: PreparedInputs) -> int:
+        """Rows per pass so that the per-row workspace (sampled scores, candidate lists, router
+        partials, MISA-dagger candidates and re-rank scores) stays within ``workspace_bytes``.
+        At C4 (128K) every method runs in one pass; at C5 (1M keys) the sample row alone is
+        64 KiB and the candidate lists 48 KiB per row, so the rows go in a few passes."""
+        kc = self.k if self.method != "misa_hier" else max(self.kprime, self.k)
+        stride, _, cap = self.selector_params(kc, x.L)
+        per_row = -(-x.L // stride) * 4 + 4 * cap * 8 + 64
+        if self.method != "dsa":
+            per_row += max(1, (x.L // self.B + 127) // 128) * x.Hp * 4 + x.Hp * 4 + 64
+        if self.method == "misa_hier":
+            per_row += 2 * kc * 4
+        rows = max(256, (self.workspace_bytes // per_row) // 256 * 256)
+        return x.T if rows >= x.T else rows
+
     def run_prepared(self, x: PreparedInputs, *, need_importance: bool = False,
                      out: torch.Tensor | None = None) -> IndexerOutput:
+        """All T rows; in row passes of ``row_chunk`` rows when the workspace would exceed
+        ``workspace_bytes`` (each pass is an independent batch of rows: same result)."""
+        if out is None:
+            out = torch.empty(x.T, self.k, dtype=torch.int32, device=x.keys.device)
+        span = self.row_chunk(x)
+        if span >= x.T:
+            return self._run_rows(x, need_importance, out)
+        res = IndexerOutput(topk=out)
+        flags = torch.empty(x.T, dtype=torch.int32, device=x.keys.device) if not self.check_overflow else None
+        nfb = 0
+        for a in range(0, x.T, span):
+            b = min(x.T, a + span)
+            r = self._run_rows(x.rows(a, b), need_importance, out[a:b])
+            nfb += r.n_fallback_rows
+            if flags is not None:
+                flags[a:b].copy_(self.last_flags[: b - a])
+            for name in ("heads", "importance", "candidates"):
+                v = getattr(r, name)
+                if v is None:
+                    continue
+                if getattr(res, name) is None:
+                    setattr(res, name, torch.empty((x.T,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device))
+                getattr(res, name)[a:b].copy_(v)
+        if flags is not None:
+            self.last_flags = flags
+        res.n_fallback_rows = nfb
+        self.last_fallback_rows = nfb
+        return res
+
+    def _run_rows(self, x: PreparedInputs, need_importance: bool, out: torch.Tensor) -> IndexerOutput:
         dev = x.keys.device
         k = self.k
-        if out is None:
-            out = torch.empty(x.T, k, dtype=torch.int32, device=dev)
         if self.method == "dsa":
             nfb = self.select(x, None, x.Hp, k, out)
             self.last_fallback_rows = nfb

@@ -210,7 +210,8 @@ def test_virtual_key_shards_decode_merge_to_single_gpu(method, G):
             xl, heads, hq, k, parts_i[r], scores=parts_s[r])
         _lib.call("misa_shard_map_indices", parts_i[r].data_ptr(), parts_i[r].numel(), B, G, r, stream)
     out = torch.empty(T, k, dtype=torch.int32, device="cuda")
-    _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, T * k, T, k, k, out.data_ptr(), k, stream)
+    _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, T * k, T, k, k, out.data_ptr(), k, None,
+              stream)
     torch.cuda.synchronize()
     assert torch.equal(out, ref.topk)
 

@@ -302,7 +302,7 @@ def test_merge_topk():
     s = torch.gather(s, -1, order)
     idx[1, 0, 5:] = -1
     out = torch.empty(T, k, dtype=torch.int32, device="cuda")
-    _lib().call("misa_merge_topk", _p(s), _p(idx), parts, T * k, T, k, k, _p(out), k, _stream())
+    _lib().call("misa_merge_topk", _p(s), _p(idx), parts, T * k, T, k, k, _p(out), k, None, _stream())
     torch.cuda.synchronize()
     for t in range(T):
         pairs = [(float(s[p, t, i]), int(idx[p, t, i])) for p in range(parts) for i in range(k) if idx[p, t, i] >= 0]
@@ -331,3 +331,60 @@ def test_refine_gather_matches_fp32():
         kk = K[cand[t, :n].long()]
         ref, mag = _dense_scores(kk, Q[t: t + 1], W[t: t + 1])
         assert ((out[t, :n].double() - ref[0]).abs() <= 1e-5 * mag[0] + 1e-6).all(), t
+
+
+def test_list_kth_prune_and_merge_rounds():
+    """Exchange-pruning kernels: misa_list_kth (m-th largest, -inf padding), misa_list_prune
+    (order-preserving compaction >= tau, counts past the cap) and merge rounds with scores
+    (sharded.merge_lists with a small capacity) == one merge of the union."""
+    from paper_2605_07363_b200 import sharded as S
+    torch.manual_seed(12)
+    R, c, m = 300, 2048, 256
+    s = (torch.randn(R, c, device="cuda") * 8).round() / 8  # ties
+    nvalid = torch.randint(0, c + 1, (R,), device="cuda")
+    nvalid[:3] = torch.tensor([0, m - 1, m], device="cuda")
+    col = torch.arange(c, device="cuda")[None]
+    s = torch.where(col < nvalid[:, None], s, torch.full_like(s, float("-inf")))
+    idx = torch.where(col < nvalid[:, None], col.int().expand(R, c) * 3, torch.full((R, c), -1, dtype=torch.int32,
+                                                                                      device="cuda"))
+    ops = S.DeviceListOps()
+    tau = ops.kth(s, m)
+    srt = torch.sort(s, dim=1, descending=True).values
+    exp_tau = torch.where(nvalid >= m, srt[:, m - 1], torch.full_like(srt[:, 0], float("-inf")))
+    assert torch.equal(tau, exp_tau)
+    cap = 400
+    ps, pi, cnt = ops.prune(s, idx, tau, cap)
+    torch.cuda.synchronize()
+    sn, ixn, tn = s.cpu().numpy(), idx.cpu().numpy(), tau.cpu().numpy()
+    psn, pin, cn = ps.cpu().numpy(), pi.cpu().numpy(), cnt.cpu().numpy()
+    for r in range(R):
+        keep = np.nonzero((ixn[r] >= 0) & (sn[r] >= tn[r]))[0]
+        assert cn[r] == keep.shape[0]
+        n = min(cap, keep.shape[0])
+        assert pin[r, :n].tolist() == ixn[r, keep[:n]].tolist() and psn[r, :n].tolist() == sn[r, keep[:n]].tolist()
+        assert (pin[r, n:] == -1).all()
+    # merge: 6 parts of disjoint ascending lists; rounds (capacity 1024) == one merge
+    P, k_in, k = 6, 600, 512
+    perm = torch.argsort(torch.rand(R, 20000, device="cuda"), dim=1)[:, : P * k_in]  # disjoint within a row
+    perm = perm.view(R, P, k_in).permute(1, 0, 2).contiguous().int()
+    pidx = torch.sort(perm, dim=2).values
+    psc = (torch.randn(P, R, k_in, device="cuda") * 4).round()
+    pidx[:, :5, 550:] = -1  # short lists
+    psc[:, :5, 550:] = float("-inf")
+    one, _ = ops.merge(psc, pidx, R, k)
+    old = S.MERGE_CAPACITY
+    try:
+        S.MERGE_CAPACITY = 1200
+        rounds = S.merge_lists(ops, psc, pidx, k)
+    finally:
+        S.MERGE_CAPACITY = old
+    torch.cuda.synchronize()
+    assert torch.equal(one, rounds)
+    sn, inn = psc.cpu().numpy(), pidx.cpu().numpy()
+    got = one.cpu().numpy()
+    for r in range(0, R, 7):
+        v, i = sn[:, r].reshape(-1), inn[:, r].reshape(-1)
+        ok = i >= 0
+        order = np.lexsort((i[ok], -v[ok]))[:k]  # (score desc, index asc)
+        exp = np.sort(i[ok][order])
+        assert got[r, : exp.shape[0]].tolist() == exp.tolist(), r

@@ -341,7 +341,7 @@ def test_virtual_key_shards_merge_to_single_gpu_result(method, G):
         _lib.call("misa_shard_map_indices", parts_i[r].data_ptr(), parts_i[r].numel(), B, G, r, stream)
     out = torch.empty((T_pad, k), dtype=torch.int32, device="cuda")
     _lib.call("misa_merge_topk", parts_s.data_ptr(), parts_i.data_ptr(), G, T_pad * k, T_pad, k, k, out.data_ptr(), k,
-              stream)
+              None, stream)
     torch.cuda.synchronize()
     assert torch.equal(out[:L], ref)
 

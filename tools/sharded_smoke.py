@@ -36,6 +36,13 @@ def worker(rank, world, port, q):
         refd = IndexerEngine(m, **kw).decode(K, Qd, Wd).topk
         gotd = ShardedIndexer(m, world=world, rank=rank, **kw).decode(K, Qd, Wd)
         ok[m + "_decode"] = bool(torch.equal(gotd, refd))
+    # MISA-dagger at k' = 8192: pruned coarse lists (m = 4096, cap 6152 per rank), full-list
+    # re-exchange of the early rows, merge of 2 x 8192 at the merge capacity
+    kw = dict(budget_k=2048, active_heads_h=8, block_size=B, candidate_kprime=8192)
+    ref = IndexerEngine("misa_hier", **kw).run(K, Q, W).topk
+    sh = ShardedIndexer("misa_hier", world=world, rank=rank, **kw)
+    ok["misa_hier_k8192_prefill"] = bool(torch.equal(sh.run(K, Q, W, gather=True), ref))
+    ok["pruned"] = sh.exchange.last.get("cols", 8192) < 8192
     q.put((rank, ok))
     dist.destroy_process_group()
 
