@@ -33,6 +33,8 @@
  *   misa_merge_topk       (no reference counterpart: key-sharded multi-GPU merge)
  *   misa_shard_map_indices (no reference counterpart: local -> global key index of a shard)
  *   misa_list_kth / misa_list_prune (no reference counterpart: pruned key-shard exchange)
+ *   misa_*_varlen         several independent key sequences / workloads in one call
+ *                         (workload.py:40-110 per workload; the reference loops over them)
  */
 #ifndef MISA_B200_H_
 #define MISA_B200_H_
@@ -86,6 +88,16 @@ int misa_route_scores(const void* queries, int64_t n_rows, int n_heads_pad, int 
                       const int32_t* it_tile, const int32_t* it_chunk, const int32_t* it_ncols, int n_items,
                       float* partial, void* stream);
 
+/* misa_route_scores over several key sequences packed with every sequence starting at a
+ * pooled-block boundary: row t's pooled blocks start at block row_boff[t] (its keys at key
+ * row_boff[t] * block_size); item i serves the rows of its tile with row_boff == it_boff[i],
+ * its chunk counted from that block. */
+int misa_route_scores_varlen(const void* queries, int64_t n_rows, int n_heads_pad, int head_dim,
+                             const void* pooled_planes, int64_t planes_rows, const float* prefix_sums,
+                             const int32_t* prefix_len, int block_size, const int32_t* it_tile,
+                             const int32_t* it_chunk, const int32_t* it_ncols, const int32_t* it_boff,
+                             const int32_t* row_boff, int n_items, float* partial, void* stream);
+
 /* K2b: importance E_tj = |w_tj| * sum_c partial / ceil(n_t/B) (block_attention), w_tj
  * (gate_only) or ||q_tj|| (query_norm); top-h heads (ties -> smaller head) ascending into
  * heads[t][0..h), -1 padded to heads_ld.  importance may be NULL. */
@@ -130,6 +142,24 @@ int misa_score_filter(const void* keys, int64_t n_keys, int head_dim, const void
                       const int32_t* prefix_len, int64_t n_rows, const int32_t* items, const int32_t* item_tiles,
                       int n_items, const float* tau, uint64_t* cand, int cap, int32_t* cand_count, void* stream);
 
+/* Several key sequences in one call (the reference's independent workloads / prefixes,
+ * workload.py:91-110, batched): work item i covers rows [item_row0[i], item_row0[i] +
+ * item_nrows[i]) (<= 256/heads_per_query rows, all of one sequence) whose keys start at key
+ * row item_key0[i] (for materialize: in units of key_stride rows); key indices in the
+ * output stay relative to the sequence.  Otherwise as misa_score_materialize / _filter. */
+int misa_score_materialize_varlen(const void* keys, int64_t n_keys, int64_t key_stride, int head_dim,
+                                  const void* queries, const float* weights, int n_heads, int n_heads_pad,
+                                  const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
+                                  int64_t n_rows, const int32_t* item_row0, const int32_t* item_nrows,
+                                  const int32_t* item_key0, const int32_t* item_tiles, int n_items, float* out,
+                                  int64_t out_ld, void* stream);
+int misa_score_filter_varlen(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                             const float* weights, int n_heads, int n_heads_pad, const int32_t* heads,
+                             int heads_per_query, const int32_t* prefix_len, int64_t n_rows,
+                             const int32_t* item_row0, const int32_t* item_nrows, const int32_t* item_key0,
+                             const int32_t* item_tiles, int n_items, const float* tau, uint64_t* cand, int cap,
+                             int32_t* cand_count, void* stream);
+
 /* Per-row threshold: tau[t] = j-th largest sampled score, j = ceil(beta*k*m/n), m = ceil(n/stride);
  * tau[t] = -inf when n <= append_all_len (every key is kept). */
 int misa_select_threshold(const float* sample_scores, int64_t ld, const int32_t* prefix_len, int64_t n_rows,
@@ -164,11 +194,13 @@ int misa_select_dense_long(const float* scores, int64_t ld, const int32_t* row_l
 
 /* MISA-dagger fine stage: out[t*out_ld + i] = sum_j w_tj ReLU(q_tj . key[cand[t][i]]) over all
  * heads, for i < n_cand[t] (cand ascending, -1 padded), for the rows listed in rows[0..n_items)
- * (longest first).  Gathered-key tcgen05 contraction (16-byte cp.async row gathers into the
+ * (longest first); with row_key0 (several key sequences, else null) row t's candidate i is key
+ * row_key0[t] + cand[t][i].  Gathered-key tcgen05 contraction (16-byte cp.async row gathers into the
  * 128-B-swizzled operand layout; completion on the stage mbarrier). */
 int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const void* queries, const float* weights,
                        int n_heads, int n_heads_pad, const int32_t* cand, int64_t cand_ld, const int32_t* n_cand,
-                       const int32_t* rows, int n_items, int64_t n_rows, float* out, int64_t out_ld, void* stream);
+                       const int32_t* rows, int n_items, int64_t n_rows, const int32_t* row_key0, float* out,
+                       int64_t out_ld, void* stream);
 
 /* Multi-GPU merge: n_parts local (score, index) top-k lists per row (parts[p][t][i], scores
  * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc).

@@ -45,8 +45,14 @@ SIGNATURES: dict[str, list] = {
     "misa_select_dense": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _vp, _vp],
     "misa_select_dense_long": [_vp, _i64, _vp, _i64, _i32, _i64, _f32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i64,
                                _vp, _vp],
-    "misa_refine_scores": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
+    "misa_refine_scores": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _vp, _i64,
                            _vp],
+    "misa_score_materialize_varlen": [_vp, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, _vp,
+                                      _vp, _vp, _i32, _vp, _i64, _vp],
+    "misa_score_filter_varlen": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp,
+                                 _i32, _vp, _vp, _i32, _vp, _vp],
+    "misa_route_scores_varlen": [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32,
+                                 _vp, _vp],
     "misa_merge_topk": [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _vp, _i64, _vp, _vp],
     "misa_list_kth": [_vp, _i64, _i64, _i32, _i32, _vp, _vp],
     "misa_list_prune": [_vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp],

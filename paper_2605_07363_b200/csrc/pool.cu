@@ -37,7 +37,11 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
   const int64_t start = (int64_t)b * B;
   const int len = (int)((start + B <= L) ? B : (L - start));
   const int sr = threadIdx.x / CH, ch = threadIdx.x % CH;
-  const int seg = (len + RP - 1) / RP;
+  // sub-segments sized from B, not from this block's length: a block's prefix sums then do
+  // not depend on how many keys follow it (a partial last block gives the same P values as
+  // the same keys followed by more keys or by zero padding, e.g. in a packed several-sequence
+  // key buffer)
+  const int seg = (B + RP - 1) / RP;
   const int s0 = sr * seg, s1 = min(len, s0 + seg);
 
   float acc[8];

@@ -27,6 +27,7 @@ struct RefineArgs {
   int64_t cand_ld;
   const int32_t* __restrict__ n_cand;
   const int32_t* __restrict__ items;  // rows, longest first
+  const int32_t* __restrict__ row_key0;  // several key sequences: row t's keys start at row_key0[t] (null: 0)
   int n_items;
   int n_keys;
   int T, H, Hp;
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
       const int nc = a.n_cand[t];
       const int nt = (nc + 127) / 128;
       const int b = it & 1;
+      const __nv_bfloat16* keys = a.keys + (a.row_key0 ? (int64_t)a.row_key0[t] * D : 0);
       if (p == 0) {
         // operands of this row: wait until the buffer's previous row is fully consumed.
         // N = max(16, Hp): rows past Hp belong to the next query row (or are zero-filled
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
         for (int i = 0; i < RPW / 2; ++i) {
           const int r = RPW * p + 2 * i + half;
           const int ki = __shfl_sync(0xffffffffu, ring[0], 2 * i + half);
-          const __nv_bfloat16* src = a.keys + (int64_t)(ki < 0 ? 0 : ki) * D + ch * 8;
+          const __nv_bfloat16* src = keys + (int64_t)(ki < 0 ? 0 : ki) * D + ch * 8;
           if (ch * 8 < D)
             cp_async16(stage + ptx::sw128_offset(r, ch * 8, C::A_ATOM), src, ki < 0 ? 0u : 16u);
         }
@@ -298,7 +300,8 @@ using namespace misa;
 extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const void* queries,
                                   const float* weights, int n_heads, int n_heads_pad, const int32_t* cand,
                                   int64_t cand_ld, const int32_t* n_cand, const int32_t* rows, int n_items,
-                                  int64_t n_rows, float* out, int64_t out_ld, void* stream) {
+                                  int64_t n_rows, const int32_t* row_key0, float* out, int64_t out_ld,
+                                  void* stream) {
   MISA_REQUIRE(keys && queries && weights && cand && n_cand && out && (rows || n_items == 0), "null pointer");
   MISA_REQUIRE(head_dim == 64 || head_dim == 128, "head_dim must be padded to 64 or 128");
   MISA_REQUIRE(n_heads >= 1 && n_heads <= n_heads_pad && n_heads_pad <= 128, "bad head counts");
@@ -320,6 +323,7 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
   a.cand_ld = cand_ld;
   a.n_cand = n_cand;
   a.items = rows;
+  a.row_key0 = row_key0;
   a.n_items = n_items;
   a.n_keys = (int)n_keys;
   a.T = (int)n_rows;

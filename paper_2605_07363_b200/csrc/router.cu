@@ -29,6 +29,10 @@ struct RouteArgs {
   const int32_t* __restrict__ it_tile;
   const int32_t* __restrict__ it_chunk;
   const int32_t* __restrict__ it_ncols;
+  // several key sequences (null: one): item i serves only the rows of its tile whose pooled
+  // blocks start at it_boff[i] (row_boff[t] == it_boff[i]); chunks are relative to that block
+  const int32_t* __restrict__ it_boff;
+  const int32_t* __restrict__ row_boff;
   int n_items;
   int T, Hp, hp_log2, B;
   int64_t planes_rows;
@@ -61,18 +65,23 @@ __device__ __forceinline__ int route_item(int it, int P, int b) { return (it & 1
 // A work item's metadata, loaded one item ahead by every role: each role walks the same
 // item list and would otherwise pay a dependent global-load round trip per tile.
 struct RouteItem {
-  int idx, chunk, ncols, tile;
+  int idx, chunk, ncols, tile, boff;
 };
 __device__ __forceinline__ RouteItem load_route_item(const RouteArgs& a, int it, int P, int b) {
   RouteItem m;
   m.idx = route_item(it, P, b);
-  m.chunk = m.ncols = m.tile = 0;
+  m.chunk = m.ncols = m.tile = m.boff = 0;
   if (m.idx < a.n_items) {
     m.chunk = __ldg(a.it_chunk + m.idx);
     m.ncols = __ldg(a.it_ncols + m.idx);
     m.tile = __ldg(a.it_tile + m.idx);
+    if (a.it_boff) m.boff = __ldg(a.it_boff + m.idx);
   }
   return m;
+}
+// Row t belongs to item m (same key sequence)?
+__device__ __forceinline__ bool route_row_in(const RouteArgs& a, const RouteItem& m, int t) {
+  return !a.row_boff || __ldg(a.row_boff + t) == m.boff;
 }
 
 template <int D>
@@ -125,9 +134,9 @@ __global__ void __launch_bounds__(192, 1)
     const int rows = 128 >> a.hp_log2;
     auto row_n = [&](const RouteItem& m) {
       const int t = m.tile * rows + lane;
-      return (m.idx < a.n_items && lane < rows && t < a.T) ? __ldg(a.prefix_len + t) : 0;
+      return (m.idx < a.n_items && lane < rows && t < a.T && route_row_in(a, m, t)) ? __ldg(a.prefix_len + t) : 0;
     };
-    int s = 0, cur_chunk = -1, nb = 0;
+    int s = 0, cur_chunk = -1, cur_boff = -1, nb = 0;
     uint32_t ph = 0;
     RouteItem nx = load_route_item(a, 0, P, bid);
     int nx_n = row_n(nx);
@@ -139,16 +148,17 @@ __global__ void __launch_bounds__(192, 1)
       nx_n = row_n(nx);
       const int chunk = cu.chunk, ncols = cu.ncols, tile = cu.tile;
       if (ncols == 0 && chunk != 0) continue;
-      if (ncols > 0 && chunk != cur_chunk) {
+      if (ncols > 0 && (chunk != cur_chunk || cu.boff != cur_boff)) {
         if (lane == 0) {
           if (nb > 0) ptx::mbar_wait(bempty, (nb - 1) & 1);
           ptx::mbar_arrive_expect_tx(bfull, C::B_BYTES);
           for (int p = 0; p < 3; ++p)
             for (int at = 0; at < D / 64; ++at)
               ptx::tma_load_2d(sB + p * C::B_PLANE + at * C::B_ATOM, &tmap_p, bfull, at * 64,
-                               (int)(p * a.planes_rows + chunk * 128));
+                               (int)(p * a.planes_rows + cu.boff + chunk * 128));
         }
         cur_chunk = chunk;
+        cur_boff = cu.boff;
         ++nb;
       }
       // chunk 0 also stages each row's partial-block prefix sum P[n-1] for the epilogue
@@ -165,13 +175,13 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 ptx::smem_u32(sP + (s * C::P_ROWS + lane) * D)),
-            "l"(a.prefix + (int64_t)(n - 1) * D), "r"(D * 4), "r"(ptx::smem_u32(&full_a[s]))
+            "l"(a.prefix + ((int64_t)cu.boff * a.B + n - 1) * D), "r"(D * 4), "r"(ptx::smem_u32(&full_a[s]))
             : "memory");
       if (++s == STAGES) { s = 0; ph ^= 1; }
     }
   } else if (warp == 1) {
     if (ptx::elect_one()) {
-      int s = 0, acc = 0, cur_chunk = -1, nb = 0;
+      int s = 0, acc = 0, cur_chunk = -1, cur_boff = -1, nb = 0;
       uint32_t ph = 0, aph = 0;
       const uint32_t b_base = ptx::smem_u32(sB);
       RouteItem nx = load_route_item(a, 0, P, bid);
@@ -187,11 +197,12 @@ __global__ void __launch_bounds__(192, 1)
           if (++s == STAGES) { s = 0; ph ^= 1; }
           continue;
         }
-        if (chunk != cur_chunk) {
+        if (chunk != cur_chunk || cu.boff != cur_boff) {
           if (nb > 0) ptx::mma_commit(bempty);  // all MMAs on the previous chunk's planes
           ptx::mbar_wait(bfull, nb & 1);
           ptx::tc_fence_after();
           cur_chunk = chunk;
+          cur_boff = cu.boff;
           ++nb;
         }
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(192, 1)
     const int lrow = quad * 32 + lane;  // A tile row = (t, j) pair
     auto row_len = [&](const RouteItem& m) {
       const int tt = (int)(((int64_t)m.tile * 128 + lrow) >> a.hp_log2);
-      return (m.idx < a.n_items && tt < a.T) ? __ldg(a.prefix_len + tt) : 0;
+      return (m.idx < a.n_items && tt < a.T && route_row_in(a, m, tt)) ? __ldg(a.prefix_len + tt) : -1;
     };
     RouteItem nx = load_route_item(a, 0, P, bid);
     int nx_n = row_len(nx);
@@ -237,13 +248,14 @@ __global__ void __launch_bounds__(192, 1)
       const int64_t grow = (int64_t)cu.tile * 128 + lrow;
       const int t = (int)(grow >> a.hp_log2);
       const int j = (int)(grow & (a.Hp - 1));
-      const int nf = n / a.B;
+      const bool mine = n >= 0;  // this row belongs to the item (n = -1: another sequence / past T)
+      const int nf = mine ? n / a.B : 0;
       // partial last block first (it needs only the A stage, not the MMA): mean over keys
       // [nf*B, n) = P[n-1] / rem, with q from the A stage
       ptx::mbar_wait(&full_a[s], ph);
       float sum = 0.f;
-      const int rem = n - nf * a.B;
-      if (t < a.T && chunk == 0 && rem > 0) {
+      const int rem = mine ? n - nf * a.B : 0;
+      if (mine && chunk == 0 && rem > 0) {
         const uint8_t* qa = sA + s * C::A_BYTES;
         const float4* pv = reinterpret_cast<const float4*>(sP + (s * C::P_ROWS + (lrow >> a.hp_log2)) * D);
         float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;  // four independent FMA chains
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       ptx::mbar_arrive(&empty_a[s]);
       if (++s == STAGES) { s = 0; ph ^= 1; }
-      if (t < a.T) a.partial[((int64_t)chunk * a.T + t) * a.Hp + j] = sum;
+      if (mine) a.partial[((int64_t)chunk * a.T + t) * a.Hp + j] = sum;
     }
   }
 
@@ -409,12 +421,12 @@ __global__ void route_select_kernel(const float* __restrict__ partial, int n_chu
 
 using namespace misa;
 
-// Work list: items (tile, chunk, ncols) precomputed on the host, chunk-major.
-extern "C" int misa_route_scores(const void* queries, int64_t n_rows, int n_heads_pad, int head_dim,
-                                 const void* pooled_planes, int64_t planes_rows, const float* prefix_sums,
-                                 const int32_t* prefix_len, int block_size, const int32_t* it_tile,
-                                 const int32_t* it_chunk, const int32_t* it_ncols, int n_items, float* partial,
-                                 void* stream) {
+// Work list: items (tile, chunk, ncols[, block offset]) precomputed on the host, chunk-major.
+extern "C" int misa_route_scores_varlen(const void* queries, int64_t n_rows, int n_heads_pad, int head_dim,
+                                        const void* pooled_planes, int64_t planes_rows, const float* prefix_sums,
+                                        const int32_t* prefix_len, int block_size, const int32_t* it_tile,
+                                        const int32_t* it_chunk, const int32_t* it_ncols, const int32_t* it_boff,
+                                        const int32_t* row_boff, int n_items, float* partial, void* stream) {
   MISA_REQUIRE(queries && pooled_planes && prefix_sums && prefix_len && partial, "null pointer");
   MISA_REQUIRE(head_dim == 64 || head_dim == 128, "head_dim must be padded to 64 or 128");
   MISA_REQUIRE(n_heads_pad >= 8 && n_heads_pad <= 128 && (n_heads_pad & (n_heads_pad - 1)) == 0,
@@ -434,6 +446,9 @@ extern "C" int misa_route_scores(const void* queries, int64_t n_rows, int n_head
   a.it_tile = it_tile;
   a.it_chunk = it_chunk;
   a.it_ncols = it_ncols;
+  a.it_boff = it_boff;
+  a.row_boff = row_boff;
+  MISA_REQUIRE((it_boff == nullptr) == (row_boff == nullptr), "it_boff and row_boff go together");
   a.n_items = n_items;
   a.T = (int)n_rows;
   a.Hp = n_heads_pad;
@@ -454,6 +469,16 @@ extern "C" int misa_route_scores(const void* queries, int64_t n_rows, int n_head
   }
   MISA_LAUNCH_CHECK();
   return MISA_OK;
+}
+
+extern "C" int misa_route_scores(const void* queries, int64_t n_rows, int n_heads_pad, int head_dim,
+                                 const void* pooled_planes, int64_t planes_rows, const float* prefix_sums,
+                                 const int32_t* prefix_len, int block_size, const int32_t* it_tile,
+                                 const int32_t* it_chunk, const int32_t* it_ncols, int n_items, float* partial,
+                                 void* stream) {
+  return misa_route_scores_varlen(queries, n_rows, n_heads_pad, head_dim, pooled_planes, planes_rows, prefix_sums,
+                                  prefix_len, block_size, it_tile, it_chunk, it_ncols, nullptr, nullptr, n_items,
+                                  partial, stream);
 }
 
 extern "C" int misa_route_select(const float* partial, int n_chunks, const float* weights, const void* queries,

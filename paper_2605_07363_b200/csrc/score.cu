@@ -134,6 +134,11 @@ struct ScoreArgs {
   const int32_t* __restrict__ item_tile0;  // MATERIALIZE key split: first tile of item i (null: 0)
   const int32_t* __restrict__ page_table;  // paged key cache: logical page -> physical page (null: flat)
   int page_tiles;                          // 128-key tiles per page
+  // several key sequences in one call (null: one sequence, item i = rows [items[i]*G, +G)):
+  // item i = rows [items[i], items[i] + item_nrows[i]) of one sequence whose keys start at
+  // key row item_key0[i] of the key buffer (key indices stay sequence-relative)
+  const int32_t* __restrict__ item_nrows;
+  const int32_t* __restrict__ item_key0;
   int n_items;
   int T, H, Hp;
   int key_stride;
@@ -233,13 +238,14 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         if (idx >= a.n_items) break;
         const int nt = a.item_tiles[idx];
         const int j0 = a.item_tile0 ? a.item_tile0[idx] : 0;
+        const int key0 = a.item_key0 ? a.item_key0[idx] : 0;
         for (int j = 0; j < nt; ++j) {
           ptx::mbar_wait(&empty_a[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full_a[s], C::A_BYTES);
           const int jj = j0 + j;  // logical tile -> row of the (possibly paged) key pool
           const int row = a.page_table ? a.page_table[jj / a.page_tiles] * (a.page_tiles * kTileKeys) +
                                              (jj % a.page_tiles) * kTileKeys
-                                       : jj * kTileKeys;
+                                       : key0 + jj * kTileKeys;
 #pragma unroll
           for (int at = 0; at < D / 64; ++at)
             ptx::tma_load_2d(sA + s * C::A_BYTES + at * C::A_ATOM, &tmap_k, &full_a[s], at * 64, row);
@@ -295,7 +301,9 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
       if (idx >= a.n_items) break;
       const int nt = a.item_tiles[idx];
       const int j0 = a.item_tile0 ? a.item_tile0[idx] : 0;
-      const int row0 = a.items[idx] * G;
+      const int row0 = a.item_nrows ? a.items[idx] : a.items[idx] * G;
+      // rows of this item: [row0, row_end) (a varlen item stops at its sequence's last row)
+      const int row_end = min(a.T, row0 + (a.item_nrows ? a.item_nrows[idx] : G));
 
       // B operand: row r = q*HQ + j <- Q[row0+q][head(q,j)][:], SW128 K-major layout.
       constexpr int CH = D / 8;  // 16-byte chunks per row
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         const int qi = col_query<HQ>(r), j = col_head<HQ>(r);
         const int row = row0 + qi;
         int head = -1;
-        if (row < a.T) head = a.heads ? a.heads[(int64_t)row * HQ + j] : (j < a.H ? j : -1);
+        if (row < row_end) head = a.heads ? a.heads[(int64_t)row * HQ + j] : (j < a.H ? j : -1);
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (head >= 0) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)row * a.Hp + head) * D + ch * 8);
         *reinterpret_cast<uint4*>(sB + ptx::sw128_offset(r, ch * 8, C::B_ATOM)) = v;
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         const int qi = col_query<HQ>(r), j = col_head<HQ>(r);
         const int row = row0 + qi;
         float wv = 0.f;
-        if (row < a.T) {
+        if (row < row_end) {
           const int head = a.heads ? a.heads[(int64_t)row * HQ + j] : (j < a.H ? j : -1);
           if (head >= 0) wv = a.w[(int64_t)row * a.Hp + head];
         }
@@ -323,10 +331,15 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
         const int row = row0 + et;
         int lim = 0;
         float tau = 0.f;
-        if (row < a.T) {
+        if (row < row_end) {
           const int n = a.prefix_len[row];
           lim = (n + a.key_stride - 1) / a.key_stride;
           if (FILTER) tau = a.tau[row];
+        } else if (FILTER) {
+          // no row here: nothing can pass (scores are finite), and the row must not pull the
+          // item's diagonal-tile bound (lim_min) down to 0
+          lim = 0x7fffffff;
+          tau = __int_as_float(0x7f800000);  // +inf
         }
         sLim[et] = lim;
         sTau[et] = tau;
@@ -410,7 +423,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
 #pragma unroll
             for (int b = 0; b < 2; ++b) {
               const int row = row0 + qa + b;
-              if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = b ? cnt_b : cnt_a;
+              if (row < row_end) a.cand_count[(int64_t)row * kQuadrants + quad] = b ? cnt_b : cnt_a;
             }
           }
         }
@@ -486,7 +499,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
             if (lane == q) mine = cnt[q];
           if (lane < QW) {
             const int row = row0 + qbase + lane;
-            if (row < a.T) a.cand_count[(int64_t)row * kQuadrants + quad] = mine;
+            if (row < row_end) a.cand_count[(int64_t)row * kQuadrants + quad] = mine;
           }
         }
       }
@@ -653,6 +666,78 @@ extern "C" int misa_score_filter(const void* keys, int64_t n_keys, int head_dim,
   a.heads = heads;
   a.prefix_len = prefix_len;
   a.items = items;
+  a.item_tiles = item_tiles;
+  a.n_items = n_items;
+  a.T = static_cast<int>(n_rows);
+  a.H = n_heads;
+  a.Hp = n_heads_pad;
+  a.key_stride = 1;
+  a.tau = tau;
+  a.cand = cand;
+  a.cap = cap;
+  a.cand_count = cand_count;
+  return dispatch_score<true>(head_dim, heads_per_query, map, a, as_stream(stream));
+}
+
+extern "C" int misa_score_materialize_varlen(const void* keys, int64_t n_keys, int64_t key_stride, int head_dim,
+                                             const void* queries, const float* weights, int n_heads, int n_heads_pad,
+                                             const int32_t* heads, int heads_per_query, const int32_t* prefix_len,
+                                             int64_t n_rows, const int32_t* item_row0, const int32_t* item_nrows,
+                                             const int32_t* item_key0, const int32_t* item_tiles, int n_items,
+                                             float* out, int64_t out_ld, void* stream) {
+  int rc = check_common(n_keys, head_dim, n_heads, n_heads_pad, heads_per_query, n_rows, keys, queries, weights,
+                        prefix_len, item_row0, item_tiles, n_items);
+  if (rc) return rc;
+  MISA_REQUIRE(n_items == 0 || (item_nrows && item_key0), "null varlen work list");
+  MISA_REQUIRE(out && out_ld >= 1 && key_stride >= 1, "null output / bad key_stride");
+  MISA_REQUIRE(heads != nullptr || heads_per_query >= n_heads, "dense scoring needs heads_per_query >= n_heads");
+  const int64_t n_sample = (n_keys + key_stride - 1) / key_stride;
+  CUtensorMap map;
+  rc = make_tmap_bf16_2d(&map, keys, head_dim, n_sample, key_stride * head_dim, kTileKeys);
+  if (rc) return rc;
+  ScoreArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.w = weights;
+  a.heads = heads;
+  a.prefix_len = prefix_len;
+  a.items = item_row0;
+  a.item_nrows = item_nrows;
+  a.item_key0 = item_key0;  // in units of the sampled key rows
+  a.item_tiles = item_tiles;
+  a.n_items = n_items;
+  a.T = static_cast<int>(n_rows);
+  a.H = n_heads;
+  a.Hp = n_heads_pad;
+  a.key_stride = static_cast<int>(key_stride);
+  a.out = out;
+  a.out_ld = out_ld;
+  return dispatch_score<false>(head_dim, heads_per_query, map, a, as_stream(stream));
+}
+
+extern "C" int misa_score_filter_varlen(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                                        const float* weights, int n_heads, int n_heads_pad, const int32_t* heads,
+                                        int heads_per_query, const int32_t* prefix_len, int64_t n_rows,
+                                        const int32_t* item_row0, const int32_t* item_nrows,
+                                        const int32_t* item_key0, const int32_t* item_tiles, int n_items,
+                                        const float* tau, uint64_t* cand, int cap, int32_t* cand_count,
+                                        void* stream) {
+  int rc = check_common(n_keys, head_dim, n_heads, n_heads_pad, heads_per_query, n_rows, keys, queries, weights,
+                        prefix_len, item_row0, item_tiles, n_items);
+  if (rc) return rc;
+  MISA_REQUIRE(n_items == 0 || (item_nrows && item_key0), "null varlen work list");
+  MISA_REQUIRE(tau && cand && cand_count && cap >= 1, "null filter buffers");
+  MISA_REQUIRE(heads != nullptr || heads_per_query >= n_heads, "dense scoring needs heads_per_query >= n_heads");
+  CUtensorMap map;
+  rc = make_tmap_bf16_2d(&map, keys, head_dim, n_keys, head_dim, kTileKeys);
+  if (rc) return rc;
+  ScoreArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.w = weights;
+  a.heads = heads;
+  a.prefix_len = prefix_len;
+  a.items = item_row0;
+  a.item_nrows = item_nrows;
+  a.item_key0 = item_key0;
   a.item_tiles = item_tiles;
   a.n_items = n_items;
   a.T = static_cast<int>(n_rows);

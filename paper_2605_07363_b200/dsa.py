@@ -111,7 +111,7 @@ def dsa_rescore(workload: IndexerWorkload, candidates, k: int, *, precision: str
     rows = torch.zeros(1, dtype=torch.int32, device="cuda")
     rs = torch.empty(1, n, dtype=torch.float32, device="cuda")
     _lib.call("misa_refine_scores", x.keys.data_ptr(), x.L, x.D, x.queries.data_ptr(), x.weights.data_ptr(), x.H,
-              x.Hp, c.data_ptr(), n, ncand.data_ptr(), rows.data_ptr(), 1, 1, rs.data_ptr(), n, _stream())
+              x.Hp, c.data_ptr(), n, ncand.data_ptr(), rows.data_ptr(), 1, 1, None, rs.data_ptr(), n, _stream())
     out = torch.empty(1, k, dtype=torch.int32, device="cuda")
     _lib.call("misa_select_dense", rs.data_ptr(), n, c.data_ptr(), n, ncand.data_ptr(), None, 1, k, out.data_ptr(), k,
               None, _stream())

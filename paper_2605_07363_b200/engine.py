@@ -77,6 +77,28 @@ class IndexerOutput:
 
 
 @dataclass
+class SeqLayout:
+    """Several independent key sequences packed in one key buffer, each starting at a
+    multiple of ``align`` key rows (``align`` is a multiple of the pooling block and of
+    the 128-key tile): row t's keys are key rows key0[t] .. key0[t] + n_t - 1, and the
+    indices it returns are relative to its own sequence.  Rows of one sequence are
+    consecutive.  This batches the reference's independent workloads
+    (``IndexerWorkload`` per query, ``workload.py:40-110``) into one device call."""
+
+    key0: torch.Tensor        # (T,) int32 device
+    key0_host: np.ndarray     # (T,) int64
+    align: int
+    block: int                # pooling block the alignment was made for (router)
+
+    def rows(self, a: int, b: int) -> "SeqLayout":
+        return SeqLayout(self.key0[a:b], self.key0_host[a:b], self.align, self.block)
+
+    @property
+    def boff(self) -> torch.Tensor:
+        return torch.div(self.key0, self.block, rounding_mode="floor").to(torch.int32)
+
+
+@dataclass
 class PreparedInputs:
     keys: torch.Tensor      # (L, D) bf16
     queries: torch.Tensor   # (T, Hp, D) bf16
@@ -91,12 +113,25 @@ class PreparedInputs:
     D: int
     causal_key: tuple | None
     pages: tuple | None = None  # paged key cache: (page_table (n_pages,) int32 device, page_size)
+    seq: SeqLayout | None = None  # several key sequences (L = the longest one)
 
     def rows(self, a: int, b: int) -> "PreparedInputs":
         """Rows [a, b) against the same key set (views, no copies)."""
         ck = None if self.causal_key is None else self.causal_key + ("rows", a, b)
         return PreparedInputs(self.keys, self.queries[a:b], self.weights[a:b], self.prefix[a:b],
-                              self.prefix_host[a:b], self.L, b - a, self.H, self.Hp, self.d, self.D, ck, self.pages)
+                              self.prefix_host[a:b], self.L, b - a, self.H, self.Hp, self.d, self.D, ck, self.pages,
+                              None if self.seq is None else self.seq.rows(a, b))
+
+    @property
+    def n_keys(self) -> int:
+        """Key rows of the key buffer (all sequences, with alignment padding)."""
+        return int(self.keys.shape[0]) if self.seq is not None else self.L
+
+    def list_key(self):
+        """Cache key of the host work lists derived from the row lengths (and sequences)."""
+        if self.causal_key is not None:
+            return self.causal_key
+        return self.prefix_host.tobytes() + (b"" if self.seq is None else self.seq.key0_host.tobytes())
 
 
 def prepare_inputs(keys, queries, weights, prefix_len=None, device=None, prefix_dev=None) -> PreparedInputs:
@@ -181,6 +216,81 @@ def paged_inputs(cache, queries, weights, prefix_len=None) -> PreparedInputs:
     prefix = torch.from_numpy(host.astype(np.int32)).to(dev)
     return PreparedInputs(cache.pool_keys, Q.contiguous(), W.contiguous(), prefix, host, L, T, H, Hp, d, D,
                           ("paged", L, T), pages=(cache.page_table, cache.B))
+
+
+def prepare_varlen(keys, cu_seqlens_k, queries, weights, cu_seqlens_q, prefix_len=None, *, block_size: int = 1024,
+                   device=None) -> PreparedInputs:
+    """Inputs of several independent sequences for one batched call.
+
+    ``keys``: (sum L_s, d) packed keys with ``cu_seqlens_k`` (S+1,) offsets; ``queries`` /
+    ``weights``: (sum T_s, H, d) / (sum T_s, H) rows of every sequence, consecutive, with
+    ``cu_seqlens_q`` (S+1,).  Row i of sequence s sees the first n keys of s: ``prefix_len``
+    per row, default causal within the sequence (n = L_s - T_s + i + 1).  A corpus of
+    single-query workloads is S sequences of T_s = 1 row with n = L_s.  The keys are copied
+    once into a buffer where every sequence starts at a multiple of lcm(block, 128) rows."""
+    ck = np.asarray(cu_seqlens_k.cpu() if isinstance(cu_seqlens_k, torch.Tensor) else cu_seqlens_k, np.int64)
+    cq = np.asarray(cu_seqlens_q.cpu() if isinstance(cu_seqlens_q, torch.Tensor) else cu_seqlens_q, np.int64)
+    if ck.ndim != 1 or cq.shape != ck.shape or ck.shape[0] < 2 or ck[0] != 0 or cq[0] != 0:
+        raise ValueError("cu_seqlens_k / cu_seqlens_q must be (S+1,) offsets starting at 0")
+    lk, lq = np.diff(ck), np.diff(cq)
+    if np.any(lk < 1) or np.any(lq < 0):
+        raise ValueError("every sequence needs >= 1 key and >= 0 query rows")
+    dev = torch.device(device) if device is not None else (
+        keys.device if isinstance(keys, torch.Tensor) and keys.is_cuda else torch.device("cuda"))
+    K = torch.as_tensor(keys, device=dev)
+    if K.ndim != 2 or K.shape[0] != ck[-1]:
+        raise ValueError(f"keys must be ({ck[-1]}, d)")
+    T = int(cq[-1])
+    if T < 1:
+        raise ValueError("need at least one query row")
+    seq_of_row = np.repeat(np.arange(lk.shape[0]), lq)
+    pos = np.arange(T) - cq[:-1][seq_of_row]
+    if prefix_len is None:
+        if np.any(lq > lk):
+            raise ValueError("causal prefill needs T_s <= L_s for every sequence")
+        host = (lk - lq)[seq_of_row] + pos + 1
+    else:
+        host = np.asarray(prefix_len.cpu() if isinstance(prefix_len, torch.Tensor) else prefix_len,
+                          np.int64).reshape(-1)
+        if host.shape[0] != T:
+            raise ValueError(f"prefix_len must have {T} entries")
+        if np.any(host < 1) or np.any(host > lk[seq_of_row]):
+            raise ValueError("prefix lengths must lie in [1, L_s] of each row's sequence")
+    align = math.lcm(int(block_size), 128)
+    padded = -(-lk // align) * align
+    off = np.concatenate([[0], np.cumsum(padded)[:-1]])
+    x = prepare_inputs(torch.zeros(1, K.shape[1], dtype=K.dtype, device=dev), queries, weights, [1] * T,
+                       device=dev)
+    Kp = torch.zeros(int(padded.sum()), x.D, dtype=torch.bfloat16, device=dev)
+    dst = torch.from_numpy(np.concatenate([np.arange(o, o + n) for o, n in zip(off, lk)])).to(dev)
+    Kp[dst, : K.shape[1]] = K.to(torch.bfloat16)
+    key0 = off[seq_of_row]
+    prefix = torch.from_numpy(host.astype(np.int32)).to(dev)
+    seq = SeqLayout(torch.from_numpy(key0.astype(np.int32)).to(dev), key0, align, int(block_size))
+    return PreparedInputs(Kp, x.queries, x.weights, prefix, host, int(lk.max()), T, x.H, x.Hp, x.d, x.D, None,
+                          None, seq)
+
+
+def varlen_groups(lens: np.ndarray, key0: np.ndarray, G: int, stride: int, min_len: int):
+    """Work items of a several-sequence call: runs of rows with the same key offset split into
+    groups of <= G rows; (row0, nrows, key0 / stride, tiles) for groups with a row longer
+    than min_len, longest first."""
+    T = lens.shape[0]
+    if np.any(key0 % stride):
+        raise ValueError(f"sequence offsets must be multiples of the sample stride {stride}")
+    run_start = np.r_[True, key0[1:] != key0[:-1]]
+    run_id = np.cumsum(run_start) - 1
+    pos = np.arange(T) - np.flatnonzero(run_start)[run_id]
+    grp = pos // G
+    g_start = np.flatnonzero(np.r_[True, (run_id[1:] != run_id[:-1]) | (grp[1:] != grp[:-1])])
+    nrows = np.diff(np.r_[g_start, T])
+    gmax = np.maximum.reduceat(lens, g_start)
+    keep = np.nonzero(gmax > min_len)[0]
+    tiles = ((gmax[keep] + stride - 1) // stride + 127) // 128
+    order = np.argsort(-tiles, kind="stable")
+    sel = keep[order]
+    return (g_start[sel].astype(np.int32), nrows[sel].astype(np.int32), (key0[g_start[sel]] // stride).astype(np.int32),
+            tiles[order].astype(np.int32))
 
 
 class IndexerEngine:
@@ -269,6 +379,26 @@ class IndexerEngine:
             cols.append(cc[order])
         return tuple(np.concatenate(x).astype(np.int32) for x in (tl, ch, cols))
 
+    def _route_items_varlen(self, lens: np.ndarray, boff: np.ndarray, Hp: int):
+        """Router items of a several-sequence call: one item per (tile, sequence in the tile,
+        chunk), the chunk counted from the sequence's first pooled block; every (tile,
+        sequence) pair has a chunk-0 item (the partial block)."""
+        T = lens.shape[0]
+        rpt = 128 // Hp
+        tile = np.arange(T) // rpt
+        nf = lens // self.B
+        # (tile, boff) pairs with the largest full-block count of their rows
+        start = np.flatnonzero(np.r_[True, (tile[1:] != tile[:-1]) | (boff[1:] != boff[:-1])])
+        p_tile, p_boff = tile[start], boff[start]
+        p_nf = np.maximum.reduceat(nf, start)
+        nch = np.maximum(1, (p_nf + 127) // 128)
+        rep = np.repeat(np.arange(start.shape[0]), nch)
+        chunk = np.arange(rep.shape[0]) - np.repeat(np.cumsum(nch) - nch, nch)
+        cols = np.clip(p_nf[rep] - 128 * chunk, 0, 128)
+        cols = (cols + 15) // 16 * 16
+        order = np.lexsort((-cols, p_boff[rep], chunk))  # chunk-major, then sequence
+        return tuple(a[order].astype(np.int32) for a in (p_tile[rep], chunk, cols, p_boff[rep]))
+
     def _dev_list(self, key, fn, device):
         def make():
             arrs = fn()
@@ -300,13 +430,16 @@ class IndexerEngine:
 
     def pool(self, x: PreparedInputs):
         """K1: in-block prefix sums + pooled planes."""
-        nf = x.L // self.B
+        nk = x.n_keys
+        nf = nk // self.B
         n_chunks = max(1, (nf + 127) // 128)
         rows = n_chunks * 128
-        P = self._buf("prefix", (x.L, x.D), torch.float32, x.keys.device)
+        P = self._buf("prefix", (nk, x.D), torch.float32, x.keys.device)
         planes = self._buf("planes", (3, rows, x.D), torch.bfloat16, x.keys.device)
         self._mark("pool")
-        _lib.call("misa_pool_keys", _ptr(x.keys), x.L, x.D, self.B, _ptr(P), None, _ptr(planes), rows, self._stream())
+        _lib.call("misa_pool_keys", _ptr(x.keys), nk, x.D, self.B, _ptr(P), None, _ptr(planes), rows, self._stream())
+        if x.seq is not None:  # chunks of the router partials count from each row's first block
+            n_chunks = max(1, (int(x.prefix_host.max()) // self.B + 127) // 128)
         return P, planes, n_chunks, rows
 
     def route(self, x: PreparedInputs, need_importance: bool = False, cache=None):
@@ -331,15 +464,26 @@ class IndexerEngine:
                 n_chunks = max(1, (x.L // self.B + 127) // 128)
             else:
                 P, planes, n_chunks, rows = self.pool(x)
-            key = ("route", x.causal_key or x.prefix_host.tobytes(), x.Hp, self.B, n_chunks)
-            it_tile, it_chunk, it_cols = self._dev_list(key, lambda: self._route_items(x.prefix_host, x.Hp, n_chunks),
-                                                        dev)
+            key = ("route", x.list_key(), x.Hp, self.B, n_chunks)
             partial = self._buf("partial", (n_chunks, x.T, x.Hp), torch.float32, dev)
-            self._mark("route_scores")
-            _lib.call("misa_route_scores", _ptr(x.queries), x.T, x.Hp, x.D, _ptr(planes), rows,
-                      P if isinstance(P, int) else _ptr(P),
-                      _ptr(x.prefix), self.B, _ptr(it_tile), _ptr(it_chunk), _ptr(it_cols), it_tile.numel(),
-                      _ptr(partial), self._stream())
+            if x.seq is None:
+                it_tile, it_chunk, it_cols = self._dev_list(
+                    key, lambda: self._route_items(x.prefix_host, x.Hp, n_chunks), dev)
+                self._mark("route_scores")
+                _lib.call("misa_route_scores", _ptr(x.queries), x.T, x.Hp, x.D, _ptr(planes), rows,
+                          P if isinstance(P, int) else _ptr(P),
+                          _ptr(x.prefix), self.B, _ptr(it_tile), _ptr(it_chunk), _ptr(it_cols), it_tile.numel(),
+                          _ptr(partial), self._stream())
+            else:
+                if x.seq.block != self.B:
+                    raise ValueError(f"sequences were aligned for block size {x.seq.block}, engine uses {self.B}")
+                it_tile, it_chunk, it_cols, it_boff = self._dev_list(
+                    key, lambda: self._route_items_varlen(x.prefix_host, x.seq.key0_host // self.B, x.Hp), dev)
+                row_boff = x.seq.boff
+                self._mark("route_scores")
+                _lib.call("misa_route_scores_varlen", _ptr(x.queries), x.T, x.Hp, x.D, _ptr(planes), rows, _ptr(P),
+                          _ptr(x.prefix), self.B, _ptr(it_tile), _ptr(it_chunk), _ptr(it_cols), _ptr(it_boff),
+                          _ptr(row_boff), it_tile.numel(), _ptr(partial), self._stream())
         self._mark("route_select")
         _lib.call("misa_route_select", _ptr(partial), n_chunks, _ptr(x.weights), _ptr(x.queries), _ptr(x.prefix),
                   x.T, x.H, x.Hp, x.D, self.B, h, kind, _ptr(heads), hq, _ptr(imp), self._stream())
@@ -356,20 +500,32 @@ class IndexerEngine:
         append_all = 4 * cap
         G = 256 // hq
         stream = self._stream()
-        ckey = x.causal_key or x.prefix_host.tobytes()
-        s_items, s_tiles = self._dev_list(("samp", ckey, G, stride, append_all),
-                                          lambda: self.group_items(x.prefix_host, G, stride, append_all), dev)
+        ckey = x.list_key()
         min_len = 0 if scores is not None else k
-        f_items, f_tiles = self._dev_list(("filt", ckey, G, min_len),
-                                          lambda: self.group_items(x.prefix_host, G, 1, min_len), dev)
+        if x.seq is None:
+            s_items, s_tiles = self._dev_list(("samp", ckey, G, stride, append_all),
+                                              lambda: self.group_items(x.prefix_host, G, stride, append_all), dev)
+            f_items, f_tiles = self._dev_list(("filt", ckey, G, min_len),
+                                              lambda: self.group_items(x.prefix_host, G, 1, min_len), dev)
+        else:
+            s_items, s_rows, s_key0, s_tiles = self._dev_list(
+                ("vsamp", ckey, G, stride, append_all),
+                lambda: varlen_groups(x.prefix_host, x.seq.key0_host, G, stride, append_all), dev)
+            f_items, f_rows, f_key0, f_tiles = self._dev_list(
+                ("vfilt", ckey, G, min_len), lambda: varlen_groups(x.prefix_host, x.seq.key0_host, G, 1, min_len), dev)
         Ls = (x.L + stride - 1) // stride
         tau = self._buf(tag + "_tau", (x.T,), torch.float32, dev)
         if s_items.numel():
             samp = self._buf(tag + "_samp", (x.T, Ls), torch.float32, dev)
             self._mark(tag + ":sample")
-            _lib.call("misa_score_materialize", _ptr(x.keys), x.L, stride, x.D, _ptr(x.queries), _ptr(x.weights),
-                      x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(s_items), _ptr(s_tiles), s_items.numel(),
-                      _ptr(samp), Ls, stream)
+            if x.seq is None:
+                _lib.call("misa_score_materialize", _ptr(x.keys), x.L, stride, x.D, _ptr(x.queries),
+                          _ptr(x.weights), x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(s_items),
+                          _ptr(s_tiles), s_items.numel(), _ptr(samp), Ls, stream)
+            else:
+                _lib.call("misa_score_materialize_varlen", _ptr(x.keys), x.n_keys, stride, x.D, _ptr(x.queries),
+                          _ptr(x.weights), x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(s_items),
+                          _ptr(s_rows), _ptr(s_key0), _ptr(s_tiles), s_items.numel(), _ptr(samp), Ls, stream)
         else:
             samp = self._buf(tag + "_samp", (1, 1), torch.float32, dev)
         self._mark(tag + ":threshold")
@@ -379,9 +535,14 @@ class IndexerEngine:
         cnt = self._buf(tag + "_cnt", (x.T * 4,), torch.int32, dev)
         if f_items.numel():
             self._mark(tag + ":filter")
-            _lib.call("misa_score_filter", _ptr(x.keys), x.L, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
-                      _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(f_items), _ptr(f_tiles), f_items.numel(), _ptr(tau),
-                      _ptr(cand), cap, _ptr(cnt), stream)
+            if x.seq is None:
+                _lib.call("misa_score_filter", _ptr(x.keys), x.L, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
+                          _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(f_items), _ptr(f_tiles), f_items.numel(),
+                          _ptr(tau), _ptr(cand), cap, _ptr(cnt), stream)
+            else:
+                _lib.call("misa_score_filter_varlen", _ptr(x.keys), x.n_keys, x.D, _ptr(x.queries), _ptr(x.weights),
+                          x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(f_items), _ptr(f_rows), _ptr(f_key0),
+                          _ptr(f_tiles), f_items.numel(), _ptr(tau), _ptr(cand), cap, _ptr(cnt), stream)
         flags = self._buf(tag + "_flags", (x.T,), torch.int32, dev)
         self.last_flags = flags
         self._mark(tag + ":select")
@@ -402,12 +563,21 @@ class IndexerEngine:
         queries / gates / heads gathered), i.e. key-split dense scores on every SM and the
         long-row exact selector — one pass for all flagged rows, whatever their number."""
         dev = x.keys.device
+        if heads is not None and heads.dim() == 1:  # a raw workspace buffer
+            heads = heads[: x.T * hq].view(x.T, hq)
+        if x.seq is not None:  # one pass per sequence: the decode machinery scores one key set
+            k0 = x.seq.key0_host[rows]
+            for key0 in np.unique(k0):
+                rs = rows[k0 == key0]
+                n = int(x.prefix_host[rs].max())
+                xs = PreparedInputs(x.keys[key0: key0 + n], x.queries, x.weights, x.prefix, x.prefix_host, n, x.T,
+                                    x.H, x.Hp, x.d, x.D, None)
+                self._dense_rows(xs, heads, hq, k, out, rs, scores)
+            return
         sel = torch.from_numpy(rows.astype(np.int64)).to(dev)
         xr = PreparedInputs(x.keys, x.queries.index_select(0, sel).contiguous(),
                             x.weights.index_select(0, sel).contiguous(), x.prefix.index_select(0, sel).contiguous(),
                             x.prefix_host[rows], x.L, int(rows.shape[0]), x.H, x.Hp, x.d, x.D, None, x.pages)
-        if heads is not None and heads.dim() == 1:  # a raw workspace buffer
-            heads = heads[: x.T * hq].view(x.T, hq)
         hr = None if heads is None else heads.index_select(0, sel).contiguous()
         o = torch.empty((xr.T, k), dtype=torch.int32, device=dev)
         so = None if scores is None else torch.empty((xr.T, k), dtype=torch.float32, device=dev)
@@ -420,7 +590,7 @@ class IndexerEngine:
         """K5 + dense select within candidates (MISA-dagger fine stage)."""
         dev = x.keys.device
         kp = cand.shape[1]
-        ckey = x.causal_key or x.prefix_host.tobytes()
+        ckey = x.list_key()
         # the candidate count of row t is min(n_t, k'), taken from the device prefix lengths:
         # under a CUDA graph (DecodeGraph) the host lengths are the bucket's, not the cache's
         ncand = self._buf("refine_ncand", (x.T,), torch.int32, dev)
@@ -431,8 +601,9 @@ class IndexerEngine:
         rs = self._buf("refine_scores", (x.T, kp), torch.float32, dev)
         stream = self._stream()
         self._mark("refine")
-        _lib.call("misa_refine_scores", _ptr(x.keys), x.L, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
-                  _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(rows), rows.numel(), x.T, _ptr(rs), kp, stream)
+        _lib.call("misa_refine_scores", _ptr(x.keys), x.n_keys, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
+                  _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(rows), rows.numel(), x.T,
+                  None if x.seq is None else _ptr(x.seq.key0), _ptr(rs), kp, stream)
         self._mark("refine_select")
         _lib.call("misa_select_dense", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), None, x.T, k,
                   _ptr(out), out.stride(0), None, stream)
@@ -464,7 +635,7 @@ class IndexerEngine:
         """(T, L) f32 score rows (valid up to each prefix), key-axis split across the SMs."""
         dev = x.keys.device
         G = 256 // hq
-        ckey = x.causal_key or x.prefix_host.tobytes()
+        ckey = x.list_key()
         target = 4 * _lib.load().misa_sm_count()
         items, tiles, tile0 = self._dev_list(("split", ckey, G, target),
                                              lambda: self.split_items(x.prefix_host, G, target), dev)
@@ -652,6 +823,13 @@ class IndexerEngine:
     def run(self, keys, queries, weights, prefix_len=None, *, need_importance: bool = False,
             out: torch.Tensor | None = None) -> IndexerOutput:
         x = prepare_inputs(keys, queries, weights, prefix_len)
+        return self.run_prepared(x, need_importance=need_importance, out=out)
+
+    def run_varlen(self, keys, cu_seqlens_k, queries, weights, cu_seqlens_q, prefix_len=None, *,
+                   need_importance: bool = False, out: torch.Tensor | None = None) -> IndexerOutput:
+        """Rows of several independent sequences in one call (see ``prepare_varlen``); the
+        returned token indices are relative to each row's own sequence."""
+        x = prepare_varlen(keys, cu_seqlens_k, queries, weights, cu_seqlens_q, prefix_len, block_size=self.B)
         return self.run_prepared(x, need_importance=need_importance, out=out)
 
     def row_chunk(self, x: PreparedInputs) -> int:

@@ -324,7 +324,7 @@ def test_refine_gather_matches_fp32():
     rows = torch.argsort(ncand, descending=True).int()
     out = torch.full((T, kp), float("nan"), device="cuda")
     _lib().call("misa_refine_scores", _p(K), L, D, _p(Q), _p(W), H, H, _p(cand), kp, _p(ncand), _p(rows), T, T,
-                _p(out), kp, _stream())
+                None, _p(out), kp, _stream())
     torch.cuda.synchronize()
     for t in range(T):
         n = int(ncand[t])
