@@ -35,6 +35,8 @@
  *   misa_list_kth / misa_list_prune (no reference counterpart: pruned key-shard exchange)
  *   misa_*_varlen         several independent key sequences / workloads in one call
  *                         (workload.py:40-110 per workload; the reference loops over them)
+ *   misa_relevance_dots   dsa.py:18-34       relevance_dots (raw per-query dot products)
+ *   misa_pack_rows_f64    workload.py:202-254 load_workload payload (f64) -> device bf16 layouts
  */
 #ifndef MISA_B200_H_
 #define MISA_B200_H_
@@ -201,6 +203,20 @@ int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const voi
                        int n_heads, int n_heads_pad, const int32_t* cand, int64_t cand_ld, const int32_t* n_cand,
                        const int32_t* rows, int n_items, int64_t n_rows, const int32_t* row_key0, float* out,
                        int64_t out_ld, void* stream);
+
+/* Raw query.key dot products (dsa.py:18-34 relevance_dots): out[i*out_ld + j] = q_j . key[i]
+ * for keys i < n_keys and query rows j < n_queries (<= 128; queries bf16 [n_queries_pad][D],
+ * n_queries_pad a power of two in [8, 128], pad rows zero).  The refine kernel's tcgen05
+ * contraction over contiguous key tiles, with an epilogue that stores the accumulator. */
+int misa_relevance_dots(const void* keys, int64_t n_keys, int head_dim, const void* queries, int n_queries,
+                        int n_queries_pad, float* out, int64_t out_ld, void* stream);
+
+/* Archived workloads (MISAWKLD, workload.py:202-254) -> device layouts: src (n_rows, d) f64 rows
+ * are rounded to bf16 into dst [.][D] (columns d..D-1 zeroed), src row r landing on row
+ * dst_row0 + (r / group) * dst_group_stride + r % group; *n_inexact (optional, accumulated)
+ * counts elements bf16 does not represent exactly. */
+int misa_pack_rows_f64(const double* src, int64_t n_rows, int d, int64_t group, int64_t dst_group_stride, void* dst,
+                       int D, int64_t dst_row0, unsigned long long* n_inexact, void* stream);
 
 /* Multi-GPU merge: n_parts local (score, index) top-k lists per row (parts[p][t][i], scores
  * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc).

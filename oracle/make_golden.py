@@ -23,6 +23,7 @@ import os
 import sys
 
 import numpy as np
+import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
@@ -142,6 +143,52 @@ def pooling_and_needles():
     print("[golden] pooling + needles")
 
 
+def archived_corpus():
+    """A small MISAWKLD corpus written by the REFERENCE's own save_workload (tests/golden/corpus/),
+    with the reference estimators' selections on it (fast32 and reference64).  Values are
+    bf16-rounded before saving (the device contract is exact on them); the needle workload
+    keeps the reference generator's layout."""
+    cdir = os.path.join(OUT, "corpus")
+    os.makedirs(cdir, exist_ok=True)
+    for f in os.listdir(cdir):
+        os.remove(os.path.join(cdir, f))
+    cfg = misa.IndexerConfig(n_heads=16, head_dim=32, budget_k=128, block_size=128, active_heads_h=4,
+                             candidate_kprime=512)
+    bf = lambda a: np.asarray(torch.from_numpy(np.asarray(a)).to(torch.bfloat16).double())  # noqa: E731
+    specs = [("random", 21, 300), ("random", 22, 900), ("needle", 23, 1800), ("random", 24, 2100)]
+    names, out = [], {}
+    for i, (kind, seed, L) in enumerate(specs):
+        if kind == "random":
+            w = misa.gen_random_workload(seed, L, cfg)
+        else:
+            w = misa.gen_needle_workload(seed, L, 0.4, 32, 10.0, cfg, noise_scale=0.01)
+        w = misa.IndexerWorkload(keys=bf(w.keys), queries=bf(w.queries),
+                                 gate_weights=np.asarray(w.gate_weights, np.float32).astype(np.float64), seed=seed)
+        name = f"workload_L{L}_d0_r{i}_s{seed}.bin"
+        misa.save_workload(w, os.path.join(cdir, name))
+        names.append(name)
+        for prec in ("fast32", "reference64"):
+            kw = dict(budget_k=cfg.budget_k, precision_mode=prec)
+            rk = dict(kw, active_heads_h=cfg.active_heads_h, block_size=cfg.block_size)
+            r_d = misa.DSAIndexer(**kw).select(w)
+            r_m = misa.MISAIndexer(**rk).select(w)
+            r_h = misa.HierarchicalMISAIndexer(**rk, candidate_kprime=cfg.candidate_kprime).select(w)
+            out[f"{prec}_dsa{i}"] = r_d.selection.indices
+            out[f"{prec}_misa{i}"] = r_m.selection.indices
+            out[f"{prec}_heads{i}"] = r_m.heads.head_indices
+            out[f"{prec}_hier{i}"] = r_h.selection.indices
+            out[f"{prec}_hier_cand{i}"] = r_h.candidates.indices
+            for tag, r in (("dsa", r_d), ("misa", r_m), ("hier", r_h)):
+                lg = r.ledger
+                out[f"{prec}_ledger_{tag}{i}"] = np.array(
+                    [lg.token_dot_products, lg.block_dot_products, lg.refine_dot_products], np.int64)
+    out["names"] = np.array(names)
+    out["cfg"] = np.array([cfg.n_heads, cfg.head_dim, cfg.budget_k, cfg.block_size, cfg.active_heads_h,
+                           cfg.candidate_kprime], np.int64)
+    np.savez_compressed(os.path.join(cdir, "reference_selections.npz"), **out)
+    print(f"[golden] corpus: {len(names)} MISAWKLD files")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     only = sys.argv[1:]
@@ -150,3 +197,5 @@ if __name__ == "__main__":
             run_case(name, *args)
     if not only or "pooling" in only:
         pooling_and_needles()
+    if not only or "corpus" in only:
+        archived_corpus()

@@ -11,7 +11,7 @@ a CUDA device.  The batched performance path is ``IndexerEngine`` /
 """
 
 from .config import (BASELINE_BLOCK_SIZE, BLOCK_ATTENTION, FAST32, GATE_ONLY, PRECISION_MODES, QUERY_NORM,
-                     REFERENCE64, ROUTER_BLOCK_SIZE, ROUTER_SCORE_KINDS, IndexerConfig, dtype_for)
+                     REFERENCE64, ROUTER_BLOCK_SIZE, ROUTER_SCORE_KINDS, IndexerConfig, PrecisionWarning, dtype_for)
 from .types import CostEntry, CostLedger, HeadSet, ScoreVector, SelectionResult, TokenSelection
 from .workload import (IndexerWorkload, NeedleLabel, gen_needle_workload, gen_random_workload, load_workload,
                        save_workload, softmax)
@@ -20,13 +20,14 @@ from .engine import DecodeGraph, IndexerEngine, IndexerOutput, prepare_inputs
 from .pooling import BlockSummary, PagedKeyCache, PooledKeyCache, build_block_summary, incremental_append
 from .dsa import dsa_rescore, dsa_score, dsa_select, gated_relu_scores, relevance_dots, topk_tokens, topk_within
 from .routing import misa_hier_select, misa_score, misa_select, route_head_importance, route_topk_heads
+from .corpus import Corpus, read_header, save_corpus, select_corpus
 from .estimators import (INDEXER_REGISTRY, METHODS, BaseTokenIndexer, DSAIndexer, HierarchicalMISAIndexer,
                          MISAIndexer, make_indexer)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "DecodeGraph", "PagedKeyCache",
+    "Corpus", "DecodeGraph", "PagedKeyCache", "PrecisionWarning", "read_header", "save_corpus", "select_corpus",
     "BASELINE_BLOCK_SIZE", "BLOCK_ATTENTION", "BaseTokenIndexer", "BlockSummary", "CostEntry", "CostLedger",
     "DSAIndexer", "FAST32", "GATE_ONLY", "HeadSet", "HierarchicalMISAIndexer", "INDEXER_REGISTRY", "IndexerConfig",
     "IndexerEngine", "IndexerOutput", "IndexerWorkload", "METHODS", "MISAIndexer", "NeedleLabel", "PRECISION_MODES",

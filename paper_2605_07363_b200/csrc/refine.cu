@@ -33,6 +33,7 @@ struct RefineArgs {
   int T, H, Hp;
   float* out;
   int64_t out_ld;
+  int dots_tiles;  // DOTS mode: 128-key tiles per work item (item i covers keys from i * 128 * dots_tiles)
 };
 
 constexpr int kRefSets = 4;                              // epilogue warp sets = TMEM accumulators
@@ -75,7 +76,10 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
 }
 
-template <int D, int N>
+// DOTS = false: MISA-dagger re-score of gathered candidates (one work item = one query row).
+// DOTS = true : relevance_dots (dsa.py:18-34): query row set 0 against contiguous keys, one work
+//               item = a run of dots_tiles key tiles, the epilogue stores the raw accumulator.
+template <int D, int N, bool DOTS>
 __global__ void __launch_bounds__(kRefThreads, 1)
     refine_kernel(const __grid_constant__ CUtensorMap tmap_q, const RefineArgs a) {
   using C = RefineCfg<D, N>;
@@ -120,6 +124,17 @@ __global__ void __launch_bounds__(kRefThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto item_at = [&](int it) { return (it & 1) ? (it + 1) * P - 1 - bid : it * P + bid; };
+  // (query row, candidate count, first key) of work item idx
+  auto item_row = [&](int idx) { return DOTS ? 0 : a.items[idx]; };
+  auto item_count = [&](int idx) {
+    if constexpr (DOTS) {
+      const int64_t k0 = (int64_t)idx * 128 * a.dots_tiles;
+      const int64_t rem = a.n_keys - k0;
+      return (int)(rem < 128 * a.dots_tiles ? rem : 128 * a.dots_tiles);
+    } else {
+      return a.n_cand[a.items[idx]];
+    }
+  };
 
   if (warp < kRefProd) {
     // ---------------------------------------------------------------- producers
@@ -132,32 +147,35 @@ __global__ void __launch_bounds__(kRefThreads, 1)
     for (int it = 0;; ++it) {
       const int idx = item_at(it);
       if (idx >= a.n_items) break;
-      const int t = a.items[idx];
-      const int nc = a.n_cand[t];
+      const int t = item_row(idx);
+      const int nc = item_count(idx);
       const int nt = (nc + 127) / 128;
       const int b = it & 1;
-      const __nv_bfloat16* keys = a.keys + (a.row_key0 ? (int64_t)a.row_key0[t] * D : 0);
+      const __nv_bfloat16* keys =
+          a.keys + (DOTS ? (int64_t)idx * 128 * a.dots_tiles * D : (a.row_key0 ? (int64_t)a.row_key0[t] * D : 0));
       if (p == 0) {
         // operands of this row: wait until the buffer's previous row is fully consumed.
         // N = max(16, Hp): rows past Hp belong to the next query row (or are zero-filled
         // past the end) and meet zero weights, so they contribute exactly 0
         ptx::mbar_wait(&bempty[b], ((it >> 1) & 1) ^ 1);
         if (lane == 0) {
-          ptx::mbar_arrive_expect_tx(&bfull[b], C::B_BYTES + a.Hp * 4);
+          ptx::mbar_arrive_expect_tx(&bfull[b], C::B_BYTES + (DOTS ? 0 : a.Hp * 4));
 #pragma unroll
           for (int at = 0; at < D / 64; ++at)
             ptx::tma_load_2d(sB + b * C::B_STRIDE + at * C::B_ATOM, &tmap_q, &bfull[b], at * 64, t * a.Hp);
-          ptx::bulk_g2s(sW + b * N, a.w + (int64_t)t * a.Hp, a.Hp * 4, &bfull[b]);
+          if (!DOTS) ptx::bulk_g2s(sW + b * N, a.w + (int64_t)t * a.Hp, a.Hp * 4, &bfull[b]);
         }
       }
-      const int32_t* cr = a.cand + (int64_t)t * a.cand_ld;
+      const int32_t* cr = DOTS ? nullptr : a.cand + (int64_t)t * a.cand_ld;
+      // candidate i's key (DOTS: the i-th key of the item's run)
+      auto cand_at = [&](int i) { return DOTS ? i : __ldg(cr + i); };
       // lane (< RPW) holds the index of tile row RPW p + lane, kIdxAhead tiles ahead
       constexpr int kIdxAhead = 4;
       int ring[kIdxAhead];
 #pragma unroll
       for (int d = 0; d < kIdxAhead; ++d) {
         const int i = d * 128 + RPW * p + lane;
-        ring[d] = (d < nt && lane < RPW && i < nc) ? __ldg(cr + i) : -1;
+        ring[d] = (d < nt && lane < RPW && i < nc) ? cand_at(i) : -1;
       }
       for (int j = 0; j < nt; ++j) {
         ptx::mbar_wait(&empty_a[s], ph ^ 1);
@@ -174,7 +192,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
 #pragma unroll
         for (int d = 0; d + 1 < kIdxAhead; ++d) ring[d] = ring[d + 1];
         const int i = (j + kIdxAhead) * 128 + RPW * p + lane;
-        ring[kIdxAhead - 1] = (j + kIdxAhead < nt && lane < RPW && i < nc) ? __ldg(cr + i) : -1;
+        ring[kIdxAhead - 1] = (j + kIdxAhead < nt && lane < RPW && i < nc) ? cand_at(i) : -1;
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
@@ -188,8 +206,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
       for (int it = 0;; ++it) {
         const int idx = item_at(it);
         if (idx >= a.n_items) break;
-        const int t = a.items[idx];
-        const int nt = (a.n_cand[t] + 127) / 128;
+        const int nt = (item_count(idx) + 127) / 128;
         const int b = it & 1;
         ptx::mbar_wait(&bfull[b], (it >> 1) & 1);
         ptx::tc_fence_after();
@@ -224,8 +241,8 @@ __global__ void __launch_bounds__(kRefThreads, 1)
     for (int it = 0;; ++it) {
       const int idx = item_at(it);
       if (idx >= a.n_items) break;
-      const int t = a.items[idx];
-      const int nc = a.n_cand[t];
+      const int t = item_row(idx);
+      const int nc = item_count(idx);
       const int nt = (nc + 127) / 128;
       const int b = it & 1;
       const int first = (set - g % kRefSets + kRefSets) % kRefSets;  // this set's first tile in the row
@@ -237,6 +254,32 @@ __global__ void __launch_bounds__(kRefThreads, 1)
           ptx::mbar_wait(&tfull[set], (gg / kRefSets) & 1);
           ptx::tc_fence_after();
           const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + set * N;
+          if constexpr (DOTS) {
+            // raw accumulator row of key i: N query columns, the first H stored
+            const int i = j * 128 + quad * 32 + lane;
+            float* orow = a.out + ((int64_t)idx * 128 * a.dots_tiles + i) * a.out_ld;
+            uint32_t r[32];
+#pragma unroll
+            for (int c = 0; c < N; c += (N < 32 ? 16 : 32)) {
+              if constexpr (N >= 32) {
+                ptx::tmem_ld_x32p(taddr + c, r);
+                ptx::tmem_wait_ld_dep32p(r);
+              } else {
+                ptx::tmem_ld_x16(taddr + c, r);
+                ptx::tmem_wait_ld_dep16(r);
+              }
+              if (c + (N < 32 ? 16 : 32) >= N) {
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[set]);
+              }
+              if (i < nc) {
+#pragma unroll
+                for (int jj = 0; jj < (N < 32 ? 16 : 32); ++jj)
+                  if (c + jj < a.H) orow[c + jj] = __uint_as_float(r[jj]);
+              }
+            }
+            continue;
+          }
           // same head order / accumulators as the dense scorer (score.cu reduce16, HQ > 16;
           // gate_relu4), so an all-head re-score reproduces the dense DSA score bit for bit
           float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
@@ -281,10 +324,10 @@ __global__ void __launch_bounds__(kRefThreads, 1)
   }
 }
 
-template <int D, int N>
+template <int D, int N, bool DOTS = false>
 static int launch_refine_t(const CUtensorMap& mq, const RefineArgs& a, cudaStream_t st) {
   using C = RefineCfg<D, N>;
-  auto kern = refine_kernel<D, N>;
+  auto kern = refine_kernel<D, N, DOTS>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
   const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
   if (grid <= 0) return MISA_OK;
@@ -345,5 +388,51 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
   MISA_REFINE_CASE(64, 128)
 #undef MISA_REFINE_CASE
   set_error("unsupported refine shape head_dim=%d heads=%d", head_dim, N);
+  return MISA_EUNSUPPORTED;
+}
+
+extern "C" int misa_relevance_dots(const void* keys, int64_t n_keys, int head_dim, const void* queries, int n_queries,
+                                   int n_queries_pad, float* out, int64_t out_ld, void* stream) {
+  MISA_REQUIRE(keys && queries && out, "null pointer");
+  MISA_REQUIRE(head_dim == 64 || head_dim == 128, "head_dim must be padded to 64 or 128");
+  MISA_REQUIRE(n_queries >= 1 && n_queries <= n_queries_pad, "bad query counts");
+  MISA_REQUIRE(n_queries_pad == 8 || n_queries_pad == 16 || n_queries_pad == 32 || n_queries_pad == 64 ||
+                   n_queries_pad == 128, "n_queries_pad must be a power of two in [8, 128]");
+  MISA_REQUIRE(out_ld >= n_queries, "out_ld < n_queries");
+  MISA_REQUIRE(n_keys >= 1 && n_keys < (int64_t(1) << 31) - 1, "bad key count");
+  MISA_REQUIRE((reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(queries) & 15) == 0,
+               "keys / queries must be 16-byte aligned");
+  CUtensorMap mq;
+  const int N = n_queries_pad < 16 ? 16 : n_queries_pad;
+  // the B box holds N rows: with 8 padded query rows the box reads 8 rows past the set, so
+  // the map covers exactly the caller's rows and TMA zero-fills the rest
+  const int rc = make_tmap_bf16_2d(&mq, queries, head_dim, n_queries_pad, head_dim, N);
+  if (rc) return rc;
+  RefineArgs a{};
+  a.keys = static_cast<const __nv_bfloat16*>(keys);
+  a.n_keys = (int)n_keys;
+  a.T = 1;
+  a.H = n_queries;
+  a.Hp = n_queries_pad;
+  a.out = out;
+  a.out_ld = out_ld;
+  // enough items to fill every SM at least once, >= 4 tiles each
+  const int64_t tiles = (n_keys + 127) / 128;
+  int per = (int)((tiles + sm_count() - 1) / sm_count());
+  a.dots_tiles = per < 4 ? 4 : per;
+  a.n_items = (int)((tiles + a.dots_tiles - 1) / a.dots_tiles);
+  cudaStream_t st = as_stream(stream);
+#define MISA_DOTS_CASE(DD, NN) \
+  if (head_dim == DD && N == NN) return launch_refine_t<DD, NN, true>(mq, a, st);
+  MISA_DOTS_CASE(128, 16)
+  MISA_DOTS_CASE(128, 32)
+  MISA_DOTS_CASE(128, 64)
+  MISA_DOTS_CASE(128, 128)
+  MISA_DOTS_CASE(64, 16)
+  MISA_DOTS_CASE(64, 32)
+  MISA_DOTS_CASE(64, 64)
+  MISA_DOTS_CASE(64, 128)
+#undef MISA_DOTS_CASE
+  set_error("unsupported relevance_dots shape head_dim=%d queries=%d", head_dim, N);
   return MISA_EUNSUPPORTED;
 }

@@ -13,8 +13,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .config import REFERENCE64, dtype_for
-from .engine import IndexerEngine, head_dim_pad, heads_pad, heads_per_query, prepare_inputs
+from .config import REFERENCE64, dtype_for, warn_if_rounded
+from .engine import head_dim_pad, heads_pad, heads_per_query, prepare_inputs, shared_engine
 from .types import CostEntry, CostLedger, ScoreVector, SelectionResult, TokenSelection
 from .validation import check_positive_int
 from .workload import IndexerWorkload
@@ -50,10 +50,31 @@ def device_scores(keys, queries, gates, heads=None) -> np.ndarray:
 
 
 def relevance_dots(keys, queries, dtype=np.float32) -> np.ndarray:
-    """(N, R) query-key dots on bf16 operands with f32 accumulation (``dsa.py:18-34``)."""
-    q = torch.as_tensor(np.asarray(queries, dtype=np.float64), device="cuda").to(torch.bfloat16).float()
-    k = torch.as_tensor(np.asarray(keys, dtype=np.float64), device="cuda").to(torch.bfloat16).float()
-    return (q @ k.T).double().cpu().numpy()
+    """(N, R) query-key dots on bf16 operands with f32 accumulation (``dsa.py:18-34``).
+
+    ``misa_relevance_dots``: the tcgen05 contraction of the refine kernel over contiguous key
+    tiles, 128 query rows per launch, the raw accumulator stored."""
+    keys = np.asarray(keys, dtype=np.float64)
+    queries = np.asarray(queries, dtype=np.float64)
+    if keys.ndim != 2 or queries.ndim != 2 or keys.shape[1] != queries.shape[1]:
+        raise ValueError("keys must be (R, d) and queries (N, d) with the same d")
+    R, d = keys.shape
+    N = queries.shape[0]
+    if R == 0 or N == 0:
+        return np.zeros((N, R))
+    D = head_dim_pad(d)
+    K = torch.zeros(R, D, dtype=torch.bfloat16, device="cuda")
+    K[:, :d] = torch.from_numpy(keys).cuda().to(torch.bfloat16)
+    out = np.empty((N, R))
+    for a in range(0, N, 128):
+        n = min(128, N - a)
+        npad = heads_pad(n)
+        Qc = torch.zeros(npad, D, dtype=torch.bfloat16, device="cuda")
+        Qc[:n, :d] = torch.from_numpy(queries[a:a + n]).cuda().to(torch.bfloat16)
+        o = torch.empty(R, n, dtype=torch.float32, device="cuda")
+        _lib.call("misa_relevance_dots", K.data_ptr(), R, D, Qc.data_ptr(), n, npad, o.data_ptr(), n, _stream())
+        out[a:a + n] = o.double().cpu().numpy().T
+    return out
 
 
 def gated_relu_scores(keys, queries, gate_weights, dtype=np.float32) -> np.ndarray:
@@ -63,23 +84,43 @@ def gated_relu_scores(keys, queries, gate_weights, dtype=np.float32) -> np.ndarr
 
 def dsa_score(workload: IndexerWorkload, *, precision: str = REFERENCE64) -> ScoreVector:
     dtype_for(precision)
+    warn_if_rounded(workload, precision)
     return ScoreVector(device_scores(workload.keys, workload.queries, workload.gate_weights), "token")
 
 
 def _select_dense_row(values: np.ndarray, k: int, idx: np.ndarray | None = None) -> np.ndarray:
-    vals = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float32), device="cuda")[None]
-    n = vals.shape[1]
+    """Top-min(k, n) of one score row on the device; ties -> smaller position (the stable
+    argsort of ``dsa.py:74,90``); returns the positions, or ``idx`` at those positions,
+    ascending.
+
+    The register selector orders f32 keys.  Float64 scores that f32 does not represent
+    exactly are resolved exactly: f32 rounding is monotone, so every score whose f32 value
+    exceeds the k-th largest f32 value is selected and every one below it is not; only the
+    scores tied with it in f32 are re-ranked by their f64 values."""
+    v64 = np.ascontiguousarray(values, dtype=np.float64)
+    n = v64.shape[0]
     if n == 0:
         return np.empty(0, np.int64)
+    vals = torch.as_tensor(v64.astype(np.float32), device="cuda")[None]
     lens = torch.tensor([n], dtype=torch.int32, device="cuda")
     out = torch.empty(1, k, dtype=torch.int32, device="cuda")
-    ix = None
+    _lib.call("misa_select_dense", vals.data_ptr(), n, None, n, lens.data_ptr(), None, 1, k, out.data_ptr(), k, None,
+              _stream())
+    sel = out[0]
+    sel = sel[sel >= 0].long()
+    if not np.array_equal(v64.astype(np.float32).astype(np.float64), v64):
+        v32 = vals[0]
+        thr = v32[sel].min()
+        above = torch.nonzero(v32 > thr).flatten()
+        tied = torch.nonzero(v32 == thr).flatten()
+        need = int(sel.numel()) - int(above.numel())
+        if need < tied.numel():
+            vd = torch.as_tensor(v64, device="cuda")
+            tied = tied[torch.sort(vd[tied], descending=True, stable=True).indices[:need]]
+        sel = torch.sort(torch.cat([above, tied])).values
     if idx is not None:
-        ix = torch.as_tensor(np.ascontiguousarray(idx, dtype=np.int32), device="cuda")[None]
-    _lib.call("misa_select_dense", vals.data_ptr(), n, None if ix is None else ix.data_ptr(), n, lens.data_ptr(),
-              None, 1, k, out.data_ptr(), k, None, _stream())
-    o = out[0].cpu().numpy()
-    return o[o >= 0].astype(np.int64)
+        sel = torch.sort(torch.as_tensor(np.asarray(idx, dtype=np.int64), device="cuda")[sel]).values
+    return sel.cpu().numpy().astype(np.int64)
 
 
 def topk_tokens(scores, k: int) -> TokenSelection:
@@ -100,6 +141,7 @@ def topk_within(scores, candidates, k: int, prefix_len: int) -> TokenSelection:
 def dsa_rescore(workload: IndexerWorkload, candidates, k: int, *, precision: str = REFERENCE64):
     """All-head re-score of a candidate set + top-k (``dsa.py:95-115``) via the gather kernel."""
     dtype_for(precision)
+    warn_if_rounded(workload, precision)
     cand = np.asarray(candidates, dtype=np.int64)
     x = prepare_inputs(torch.tensor(workload.keys), torch.tensor(workload.queries)[None],
                        torch.tensor(workload.gate_weights)[None], [workload.prefix_len])
@@ -124,7 +166,8 @@ def dsa_select(workload: IndexerWorkload, k: int, *, precision: str = REFERENCE6
     """Dense selection: all heads score all prefix tokens, top-k (``dsa.py:118-132``)."""
     check_positive_int(k, "k")
     dtype_for(precision)
-    eng = IndexerEngine("dsa", budget_k=k)
+    warn_if_rounded(workload, precision)
+    eng = shared_engine("dsa", budget_k=k)
     res = eng.run(torch.tensor(workload.keys), torch.tensor(workload.queries)[None],
                   torch.tensor(workload.gate_weights)[None], [workload.prefix_len])
     o = res.topk[0].cpu().numpy()

@@ -901,6 +901,23 @@ class IndexerEngine:
                              candidates=cand, n_fallback_rows=nfb)
 
 
+_SHARED: dict = {}
+
+
+def shared_engine(method: str, **kw) -> IndexerEngine:
+    """One engine per (method, parameters) for the single-query API (``dsa_select``,
+    ``misa_select``, ...): its workspace and work lists are reused across calls instead of
+    being rebuilt per query.  Small LRU; not for concurrent use from several threads."""
+    key = (method, tuple(sorted(kw.items())))
+    eng = _SHARED.pop(key, None)
+    if eng is None:
+        eng = IndexerEngine(method, **kw)
+        while len(_SHARED) >= 8:
+            _SHARED.pop(next(iter(_SHARED)))
+    _SHARED[key] = eng
+    return eng
+
+
 class DecodeGraph:
     """Per-token decode step replayed from a CUDA graph (serving path for configs C5).
 

@@ -11,9 +11,9 @@ import numpy as np
 import torch
 
 from . import _lib
-from .config import BLOCK_ATTENTION, REFERENCE64, ROUTER_SCORE_KINDS, IndexerConfig, dtype_for
+from .config import BLOCK_ATTENTION, REFERENCE64, ROUTER_SCORE_KINDS, IndexerConfig, dtype_for, warn_if_rounded
 from .dsa import _select_dense_row, device_scores
-from .engine import IndexerEngine, prepare_inputs
+from .engine import prepare_inputs, shared_engine
 from .pooling import BlockSummary
 from .types import CostEntry, CostLedger, HeadSet, ScoreVector, SelectionResult, TokenSelection
 from .validation import check_choice
@@ -37,9 +37,10 @@ def route_head_importance(workload: IndexerWorkload, summary: BlockSummary, kind
     """Per-head importance: block_attention mean_b |w ReLU(q . kbar_b)|, gate_only w, query_norm ||q||."""
     check_choice(kind, ROUTER_SCORE_KINDS, "kind")
     dtype_for(precision)
+    warn_if_rounded(workload, precision)
     if kind == BLOCK_ATTENTION:
         _check_router_inputs(workload, summary)
-    eng = IndexerEngine("misa", active_heads_h=1, block_size=summary.block_size, router_score=kind)
+    eng = shared_engine("misa", active_heads_h=1, block_size=summary.block_size, router_score=kind)
     x = prepare_inputs(*_one(workload))
     _, _, imp = eng.route(x, need_importance=True)
     return ScoreVector(imp[0, : workload.n_heads].double().cpu().numpy(), "head")
@@ -57,6 +58,7 @@ def route_topk_heads(importance, h: int) -> HeadSet:
 def misa_score(workload: IndexerWorkload, heads: HeadSet, *, precision: str = REFERENCE64) -> ScoreVector:
     """Per-token scores over the active heads only (``routing.py:78-99``)."""
     dtype_for(precision)
+    warn_if_rounded(workload, precision)
     if len(heads) == 0:
         raise ValueError("head set must contain at least one active head")
     if heads.n_heads != workload.n_heads:
@@ -80,9 +82,10 @@ def _ledger(workload, summary_blocks, n_heads_used, kind, refine=None):
 
 def _run(workload, summary, cfg: IndexerConfig, kind, method):
     check_choice(kind, ROUTER_SCORE_KINDS, "kind")
+    warn_if_rounded(workload, cfg.precision_mode)
     if kind == BLOCK_ATTENTION:
         _check_router_inputs(workload, summary)
-    eng = IndexerEngine(method, budget_k=cfg.budget_k, active_heads_h=cfg.active_heads_h,
+    eng = shared_engine(method, budget_k=cfg.budget_k, active_heads_h=cfg.active_heads_h,
                         block_size=summary.block_size, candidate_kprime=cfg.candidate_kprime, router_score=kind)
     return eng.run(*_one(workload))
 
