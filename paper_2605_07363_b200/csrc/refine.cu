@@ -2,19 +2,22 @@
 //
 // Row t re-scores its k' coarse candidates with ALL H heads:
 //   out[t][i] = sum_j w_{t,j} ReLU(q_{t,j} . k_{cand[t][i]})
-// The A operand is a gather of candidate key rows: four producer warps copy them
-// with 16-byte cp.async, half a warp per key row so every warp instruction moves two
-// whole rows (coalesced, no partial sectors), straight into the 128-B-swizzled K-major
-// layout the UMMA descriptor expects; completion is tracked by the stage mbarrier
-// (cp.async.mbarrier.arrive.noinc), candidate indices are prefetched tiles ahead.
-// (TMA tile::gather4 was measured slower here: its per-SM issue rate, not L2, bounds
-// 4-row gathers.)  B = the row's Hp query heads and gate weights, TMA-loaded into one
-// of two buffers so the next row's operands land while this row computes.  The
-// contraction is L2-bandwidth bound (the key set stays L2-resident: 32 MiB at 128K);
-// the epilogue runs four warp sets over a 4-deep TMEM accumulator ring.
+// The A operand is a gather of candidate key rows with 16-byte cp.async, half a warp per
+// key row so every warp instruction moves two whole rows (coalesced, no partial sectors),
+// straight into the 128-B-swizzled K-major layout the UMMA descriptor expects; completion
+// is tracked by the stage mbarrier (cp.async.mbarrier.arrive.noinc).  The gather is bound
+// by how many cp.async requests are in flight per SM, which grows with the number of
+// independent producer warps, not with stages alone (tools/ubench_gather.cu: one group of
+// 4 warps 8.5 TB/s, six groups of 2 warps 15.7 TB/s from an L2-resident table), so the
+// producers are kRefGroups independent groups: group g fills the tiles g, g + G, ... of the
+// CTA's tile sequence, prefetching its next tile's candidate indices while it issues.
+// (TMA tile::gather4 and 1-D bulk copies per row were measured slower.)  B = the row's Hp
+// query heads and gate weights, TMA-loaded by a dedicated warp into one of two buffers so
+// the next row's operands land while this row computes; the epilogue runs kRefSets warp
+// sets over a kRefAcc-deep TMEM accumulator ring.
 //
-// Warps: 0-3 producers (+ B loads), 4 MMA issuer, 5..20 epilogue (set = tile % 4,
-// TMEM lane quadrant = warp % 4).
+// Warps: [0, G*W) producers, G*W MMA issuer, G*W+1 B loader, then 4*kRefSets epilogue
+// warps (set = tile % kRefSets, TMEM lane quadrant = warp % 4).
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -36,11 +39,16 @@ struct RefineArgs {
   int dots_tiles;  // DOTS mode: 128-key tiles per work item (item i covers keys from i * 128 * dots_tiles)
 };
 
-constexpr int kRefSets = 4;                              // epilogue warp sets = TMEM accumulators
-constexpr int kRefProd = 4;                              // cp.async producer warps
+constexpr int kRefGroups = 6;                            // independent producer groups
+constexpr int kRefGroupWarps = 2;                        // warps per group (64 tile rows each)
+constexpr int kRefProd = kRefGroups * kRefGroupWarps;    // cp.async producer warps
+constexpr int kRefAcc = 4;                               // TMEM accumulators (ring)
+constexpr int kRefSets = 2;                              // epilogue warp sets (set = tile % kRefSets)
 constexpr int kRefMma = kRefProd;                        // MMA warp index
-constexpr int kRefEpi0 = kRefProd + 1;                   // first epilogue warp
-constexpr int kRefThreads = 32 * (kRefEpi0 + 4 * kRefSets);  // 672
+constexpr int kRefBLoad = kRefProd + 1;                  // B (queries + gates) loader warp
+constexpr int kRefEpi0 = kRefProd + 2;                   // first epilogue warp
+constexpr int kRefThreads = 32 * (kRefEpi0 + 4 * kRefSets);  // 704
+static_assert(kRefAcc % kRefSets == 0, "each set owns whole accumulators");
 
 template <int D, int N>
 struct RefineCfg {
@@ -49,19 +57,19 @@ struct RefineCfg {
   static constexpr int B_ATOM = N * 128;
   static constexpr int B_BYTES = B_ATOM * (D / 64);
   static constexpr int B_STRIDE = ((B_BYTES + 1023) / 1024) * 1024;
-  // as many gather stages as shared memory holds: the gather is latency x bytes-in-flight bound
-  static constexpr int STAGES_FIT = (227 * 1024 - 1024 - 2 * B_STRIDE - 2 * N * 4 - 512) / A_BYTES;
-  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  // as many gather stages as shared memory holds
+  static constexpr int STAGES_FIT = (227 * 1024 - 1024 - 2 * B_STRIDE - 2 * N * 4 - 1024) / A_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = STAGES * A_BYTES;       // 2 buffers
   static constexpr int OFF_W = OFF_B + 2 * B_STRIDE;   // 2 x N f32
   static constexpr int OFF_BAR = OFF_W + 2 * N * 4;
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * kRefSets + 4;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * kRefAcc + 4;
   static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
-  static constexpr int TMEM_COLS = (kRefSets * N <= 32) ? 32 : (kRefSets * N <= 64) ? 64 : (kRefSets * N <= 128) ? 128
-                                   : (kRefSets * N <= 256) ? 256 : 512;
-  static_assert(kRefSets * N <= 512, "TMEM accumulator ring");
+  static constexpr int TMEM_COLS = (kRefAcc * N <= 32) ? 32 : (kRefAcc * N <= 64) ? 64 : (kRefAcc * N <= 128) ? 128
+                                   : (kRefAcc * N <= 256) ? 256 : 512;
+  static_assert(kRefAcc * N <= 512, "TMEM accumulator ring");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
 
@@ -93,8 +101,8 @@ __global__ void __launch_bounds__(kRefThreads, 1)
   uint64_t* full_a = bars;
   uint64_t* empty_a = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = tfull + kRefSets;
-  uint64_t* bfull = tempty + kRefSets;  // [2]
+  uint64_t* tempty = tfull + kRefAcc;
+  uint64_t* bfull = tempty + kRefAcc;   // [2]
   uint64_t* bempty = bfull + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -103,10 +111,10 @@ __global__ void __launch_bounds__(kRefThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmap_q);
     for (int i = 0; i < STAGES; ++i) {
-      ptx::mbar_init(&full_a[i], 32 * kRefProd);  // one cp.async completion arrival per producer thread
+      ptx::mbar_init(&full_a[i], 32 * kRefGroupWarps);  // one cp.async completion arrival per group thread
       ptx::mbar_init(&empty_a[i], 1);
     }
-    for (int i = 0; i < kRefSets; ++i) {
+    for (int i = 0; i < kRefAcc; ++i) {
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 128);
     }
@@ -138,71 +146,78 @@ __global__ void __launch_bounds__(kRefThreads, 1)
 
   if (warp < kRefProd) {
     // ---------------------------------------------------------------- producers
-    // warp p covers tile rows [RPW p, RPW p + RPW): instruction i moves rows RPW p + 2i and
-    // RPW p + 2i + 1 (lanes 0-15 / 16-31, one 16-byte chunk each)
-    constexpr int RPW = 128 / kRefProd;
-    const int p = warp, half = lane >> 4, ch = lane & 15;
-    int s = 0;
-    uint32_t ph = 0;
-    for (int it = 0;; ++it) {
-      const int idx = item_at(it);
-      if (idx >= a.n_items) break;
-      const int t = item_row(idx);
-      const int nc = item_count(idx);
-      const int nt = (nc + 127) / 128;
-      const int b = it & 1;
-      const __nv_bfloat16* keys =
-          a.keys + (DOTS ? (int64_t)idx * 128 * a.dots_tiles * D : (a.row_key0 ? (int64_t)a.row_key0[t] * D : 0));
-      if (p == 0) {
-        // operands of this row: wait until the buffer's previous row is fully consumed.
-        // N = max(16, Hp): rows past Hp belong to the next query row (or are zero-filled
-        // past the end) and meet zero weights, so they contribute exactly 0
-        ptx::mbar_wait(&bempty[b], ((it >> 1) & 1) ^ 1);
-        if (lane == 0) {
-          ptx::mbar_arrive_expect_tx(&bfull[b], C::B_BYTES + (DOTS ? 0 : a.Hp * 4));
-#pragma unroll
-          for (int at = 0; at < D / 64; ++at)
-            ptx::tma_load_2d(sB + b * C::B_STRIDE + at * C::B_ATOM, &tmap_q, &bfull[b], at * 64, t * a.Hp);
-          if (!DOTS) ptx::bulk_g2s(sW + b * N, a.w + (int64_t)t * a.Hp, a.Hp * 4, &bfull[b]);
+    // group grp fills the CTA-global tiles g == grp (mod G).  Warp wi of the group covers
+    // tile rows [64 wi, 64 wi + 64): instruction i moves rows 64 wi + 2i and 2i + 1
+    // (lanes 0-15 / 16-31, one 16-byte chunk each).  Lane l holds the key indices of
+    // rows 64 wi + l and 64 wi + 32 + l, loaded one of the group's tiles ahead.
+    constexpr int RPW = 128 / kRefGroupWarps;
+    static_assert(RPW == 64, "two index registers per lane");
+    const int grp = warp / kRefGroupWarps, wi = warp % kRefGroupWarps;
+    const int half = lane >> 4, ch = lane & 15;
+    int g0 = 0;  // CTA-global index of the current item's first tile
+    // the group's tiles as (item, tile) pairs, walked in order with a one-tile index prefetch
+    int it = 0, idx = item_at(0), j = grp;
+    int nt = 0, nc = 0, t = 0;
+    const int32_t* cr = nullptr;
+    const __nv_bfloat16* keys = a.keys;
+    auto enter = [&]() {  // advance (it, j) to the group's next tile; false when done
+      for (;;) {
+        if (idx >= a.n_items) return false;
+        t = item_row(idx);
+        nc = item_count(idx);
+        nt = (nc + 127) / 128;
+        if (j < nt) {
+          cr = DOTS ? nullptr : a.cand + (int64_t)t * a.cand_ld;
+          keys = a.keys + (DOTS ? (int64_t)idx * 128 * a.dots_tiles * D
+                                : (a.row_key0 ? (int64_t)a.row_key0[t] * D : 0));
+          return true;
         }
+        j -= nt;
+        g0 += nt;
+        idx = item_at(++it);
       }
-      const int32_t* cr = DOTS ? nullptr : a.cand + (int64_t)t * a.cand_ld;
-      // candidate i's key (DOTS: the i-th key of the item's run)
-      auto cand_at = [&](int i) { return DOTS ? i : __ldg(cr + i); };
-      // lane (< RPW) holds the index of tile row RPW p + lane, kIdxAhead tiles ahead
-      constexpr int kIdxAhead = 4;
-      int ring[kIdxAhead];
+    };
+    auto load_idx = [&](int jj, int ncc, const int32_t* crr, int (&v)[2]) {
 #pragma unroll
-      for (int d = 0; d < kIdxAhead; ++d) {
-        const int i = d * 128 + RPW * p + lane;
-        ring[d] = (d < nt && lane < RPW && i < nc) ? cand_at(i) : -1;
+      for (int u = 0; u < 2; ++u) {
+        const int i = jj * 128 + RPW * wi + 32 * u + lane;
+        v[u] = i < ncc ? (DOTS ? i : __ldg(crr + i)) : -1;
       }
-      for (int j = 0; j < nt; ++j) {
+    };
+    if (enter()) {
+      int cur[2];
+      load_idx(j, nc, cr, cur);
+      for (;;) {
+        const int g = g0 + j;
+        const int s = g % STAGES;
+        const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
+        const __nv_bfloat16* kcur = keys;
+        // next tile of this group (prefetch its indices before issuing this one)
+        j += kRefGroups;
+        const bool more = enter();
+        int nxt[2] = {-1, -1};
+        if (more) load_idx(j, nc, cr, nxt);
         ptx::mbar_wait(&empty_a[s], ph ^ 1);
         uint8_t* stage = sA + s * C::A_BYTES;
 #pragma unroll
         for (int i = 0; i < RPW / 2; ++i) {
-          const int r = RPW * p + 2 * i + half;
-          const int ki = __shfl_sync(0xffffffffu, ring[0], 2 * i + half);
-          const __nv_bfloat16* src = keys + (int64_t)(ki < 0 ? 0 : ki) * D + ch * 8;
+          const int r = RPW * wi + 2 * i + half;
+          const int ki = __shfl_sync(0xffffffffu, i < 16 ? cur[0] : cur[1], (2 * i + half) & 31);
+          const __nv_bfloat16* src = kcur + (int64_t)(ki < 0 ? 0 : ki) * D + ch * 8;
           if (ch * 8 < D)
             cp_async16(stage + ptx::sw128_offset(r, ch * 8, C::A_ATOM), src, ki < 0 ? 0u : 16u);
         }
         cp_async_mbar_arrive(&full_a[s]);
-#pragma unroll
-        for (int d = 0; d + 1 < kIdxAhead; ++d) ring[d] = ring[d + 1];
-        const int i = (j + kIdxAhead) * 128 + RPW * p + lane;
-        ring[kIdxAhead - 1] = (j + kIdxAhead < nt && lane < RPW && i < nc) ? cand_at(i) : -1;
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (!more) break;
+        cur[0] = nxt[0];
+        cur[1] = nxt[1];
       }
     }
   } else if (warp == kRefMma) {
     // ---------------------------------------------------------------- MMA issuer
     if (ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, N);
-      int s = 0;
-      uint32_t ph = 0;
-      int g = 0;  // global tile counter (accumulator ring slot g % kRefSets)
+      int g = 0;  // CTA-global tile counter: stage g % STAGES, accumulator g % kRefAcc
       for (int it = 0;; ++it) {
         const int idx = item_at(it);
         if (idx >= a.n_items) break;
@@ -212,9 +227,10 @@ __global__ void __launch_bounds__(kRefThreads, 1)
         ptx::tc_fence_after();
         const uint32_t b_base = ptx::smem_u32(sB + b * C::B_STRIDE);
         for (int j = 0; j < nt; ++j, ++g) {
-          const int acc = g % kRefSets;
-          ptx::mbar_wait(&tempty[acc], ((g / kRefSets) & 1) ^ 1);
-          ptx::mbar_wait(&full_a[s], ph);
+          const int acc = g % kRefAcc;
+          const int s = g % STAGES;
+          ptx::mbar_wait(&tempty[acc], ((g / kRefAcc) & 1) ^ 1);
+          ptx::mbar_wait(&full_a[s], (g / STAGES) & 1);
           ptx::fence_proxy_async_smem();  // cp.async (generic-proxy) writes -> tensor-core reads
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(sA + s * C::A_BYTES);
@@ -228,9 +244,27 @@ __global__ void __launch_bounds__(kRefThreads, 1)
           }
           ptx::mma_commit(&empty_a[s]);
           ptx::mma_commit(&tfull[acc]);
-          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         ptx::mma_commit(&bempty[b]);  // B buffer reusable once this row's MMAs are done
+      }
+    }
+  } else if (warp == kRefBLoad) {
+    // ---------------------------------------------------------------- B loader
+    // operands of row it into buffer it & 1 once the buffer's previous row is fully consumed.
+    // N = max(16, Hp): rows past Hp belong to the next query row (or are zero-filled past the
+    // end) and meet zero weights, so they contribute exactly 0
+    if (lane == 0) {
+      for (int it = 0;; ++it) {
+        const int idx = item_at(it);
+        if (idx >= a.n_items) break;
+        const int t = item_row(idx);
+        const int b = it & 1;
+        ptx::mbar_wait(&bempty[b], ((it >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&bfull[b], C::B_BYTES + (DOTS ? 0 : a.Hp * 4));
+#pragma unroll
+        for (int at = 0; at < D / 64; ++at)
+          ptx::tma_load_2d(sB + b * C::B_STRIDE + at * C::B_ATOM, &tmap_q, &bfull[b], at * 64, t * a.Hp);
+        if (!DOTS) ptx::bulk_g2s(sW + b * N, a.w + (int64_t)t * a.Hp, a.Hp * 4, &bfull[b]);
       }
     }
   } else {
@@ -248,12 +282,15 @@ __global__ void __launch_bounds__(kRefThreads, 1)
       const int first = (set - g % kRefSets + kRefSets) % kRefSets;  // this set's first tile in the row
       if (first < nt) {
         ptx::mbar_wait(&bfull[b], (it >> 1) & 1);
+        __syncwarp();
         const float4* w4 = reinterpret_cast<const float4*>(sW + b * N);
         for (int j = first; j < nt; j += kRefSets) {
           const int gg = g + j;
-          ptx::mbar_wait(&tfull[set], (gg / kRefSets) & 1);
+          const int acc = gg % kRefAcc;
+          ptx::mbar_wait(&tfull[acc], (gg / kRefAcc) & 1);
+          __syncwarp();  // reconverge before the warp-collective TMEM loads
           ptx::tc_fence_after();
-          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + set * N;
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * N;
           if constexpr (DOTS) {
             // raw accumulator row of key i: N query columns, the first H stored
             const int i = j * 128 + quad * 32 + lane;
@@ -270,7 +307,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
               }
               if (c + (N < 32 ? 16 : 32) >= N) {
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&tempty[set]);
+                ptx::mbar_arrive(&tempty[acc]);
               }
               if (i < nc) {
 #pragma unroll
@@ -283,7 +320,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
           // same head order / accumulators as the dense scorer (score.cu reduce16, HQ > 16;
           // gate_relu4), so an all-head re-score reproduces the dense DSA score bit for bit
           float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-          uint32_t r[N < 32 ? 32 : 32];
+          uint32_t r[32];
 #pragma unroll
           for (int c = 0; c < N; c += 32) {
             if constexpr (N >= 32) {
@@ -291,7 +328,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
               ptx::tmem_wait_ld_dep32p(r);
               if (c + 32 >= N) {  // the accumulator can be refilled once the last chunk is in registers
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&tempty[set]);
+                ptx::mbar_arrive(&tempty[acc]);
               }
 #pragma unroll
               for (int jj = 0; jj < 32; jj += 4) gate_relu4(s0, s1, w4[(c + jj) / 4], r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
@@ -301,7 +338,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
             ptx::tmem_ld_x16(taddr, r);
             ptx::tmem_wait_ld_dep16(r);
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[set]);
+            ptx::mbar_arrive(&tempty[acc]);
 #pragma unroll
             for (int jj = 0; jj < N; jj += 4) gate_relu4(s0, s1, w4[jj / 4], r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
           }
