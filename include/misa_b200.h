@@ -27,6 +27,8 @@
  *   misa_score_filter     dsa.py:37-76 fused with the candidate pass of topk_tokens
  *   misa_select_threshold (no reference counterpart: sampled threshold for the fused top-k)
  *   misa_select_topk      dsa.py:64-76       topk_tokens over the filtered candidates
+ *   misa_select_topk_runs routing.py:157-159 the coarse top-k' set of misa_hier_select (unordered runs)
+ *   misa_select_dense_runs dsa.py:79-92      topk_within over those runs (re-rank selection)
  *   misa_select_dense     dsa.py:64-92       topk_tokens / topk_within over a dense score row
  *   misa_select_dense_long dsa.py:64-76      topk_tokens over long dense rows (decode), all SMs
  *   misa_refine_scores    dsa.py:95-115      dsa_rescore (MISA-dagger fine stage), routing.py:144-174
@@ -193,6 +195,21 @@ int misa_select_dense_long(const float* scores, int64_t ld, const int32_t* row_l
                            int64_t max_len, float beta, float* tau, int32_t* seg_cnt, float* cand_scores,
                            int32_t* cand_idx, int32_t* cand_count, int cap, int32_t* topk, int64_t topk_ld,
                            float* topk_scores, void* stream);
+
+/* misa_select_topk with an unordered result (MISA-dagger's coarse candidates): the selected
+ * set of each row is written as kQuadrants = 4 consecutive runs, each ascending (the selected
+ * keys of quadrant list q), with their lengths in runs[t*4 + q] (16-byte aligned); padded with
+ * -1 past min(k, n).  Skips the ordering passes of the ascending output.  Flags as
+ * misa_select_topk (flagged rows: runs 0). */
+int misa_select_topk_runs(const uint64_t* cand, const int32_t* cand_count, int cap, const int32_t* prefix_len,
+                          int64_t n_rows, int k, int64_t max_prefix_len, int32_t* topk, int64_t topk_ld,
+                          int32_t* runs, int32_t* flags, void* stream);
+
+/* misa_select_dense over rows made of 4 ascending runs (runs[t*4 + q] lengths, summing to
+ * row_len[t]) with explicit indices idx: the top-k (score desc, index asc), ascending. */
+int misa_select_dense_runs(const float* scores, int64_t ld, const int32_t* idx, int64_t idx_ld,
+                           const int32_t* row_len, const int32_t* runs, int64_t n_rows, int k, int32_t* topk,
+                           int64_t topk_ld, void* stream);
 
 /* MISA-dagger fine stage: out[t*out_ld + i] = sum_j w_tj ReLU(q_tj . key[cand[t][i]]) over all
  * heads, for i < n_cand[t] (cand ascending, -1 padded), for the rows listed in rows[0..n_items)

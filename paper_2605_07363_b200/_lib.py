@@ -57,6 +57,8 @@ SIGNATURES: dict[str, list] = {
     "misa_list_kth": [_vp, _i64, _i64, _i32, _i32, _vp, _vp],
     "misa_list_prune": [_vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     "misa_shard_map_indices": [_vp, _i64, _i32, _i32, _i32, _vp],
+    "misa_select_topk_runs": [_vp, _vp, _i32, _vp, _i64, _i32, _i64, _vp, _i64, _vp, _vp, _vp],
+    "misa_select_dense_runs": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _vp],
     "misa_relevance_dots": [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _i64, _vp],
     "misa_pack_rows_f64": [_vp, _i64, _i32, _i64, _i64, _vp, _i32, _i64, _vp, _vp],
 }

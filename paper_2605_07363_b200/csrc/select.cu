@@ -1108,12 +1108,17 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) topk_kernel(const uin
 // needs no merge: the scorer's quadrant q holds exactly the 32-key chunks c = idx/32
 // with c % 4 == q, so all selected elements of a chunk are contiguous in one list and
 //   pos = #selected in chunks < c (block scan of a chunk histogram) + rank within c.
-template <int NT, int EPT, bool WS>  // WS: selected scores are returned too (topk_scores)
+// UO (unordered): the selected set is written in list-major compaction order — four runs,
+// each ascending (quadrant q's selected keys), run lengths in runs[t][0..4) — skipping the
+// chunk histogram / scan / reposition that the ascending output needs (MISA-dagger's coarse
+// candidates: the re-rank's selector merges the runs, misa_select_dense_runs).
+template <int NT, int EPT, bool WS, bool UO = false>  // WS: selected scores are returned too (topk_scores)
 __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_kernel(const uint64_t* __restrict__ cand,
                                                       const int32_t* __restrict__ cand_count, int cap,
                                                       const int32_t* __restrict__ prefix_len, int n_rows, int k,
                                                       int n_chunks, int32_t* __restrict__ topk, int64_t topk_ld,
-                                                      float* __restrict__ topk_scores, int32_t* __restrict__ flags) {
+                                                      float* __restrict__ topk_scores, int32_t* __restrict__ flags,
+                                                      int32_t* __restrict__ runs = nullptr) {
   constexpr int NW = NT / 32, WPL = NW / kQuadrants, WE = 32 * EPT;
   static_assert(NW % kQuadrants == 0, "warps split evenly over the quadrant lists");
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -1215,6 +1220,7 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
         out[i] = i < n ? i : -1;
         if (outs) outs[i] = -INFINITY;
       }
+      if (UO && tid < kQuadrants) runs[(int64_t)t * kQuadrants + tid] = tid == 0 ? max(0, min(n, k)) : 0;
       if (tid == 0 && flags) flags[t] = 0;
       __syncthreads();  // pf (next row) published before anyone reads it
       continue;
@@ -1270,6 +1276,7 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
         load_meta(t + 2 * gridDim.x);
       }
       for (int i = tid; i < k; i += NT) out[i] = -1;
+      if (UO && tid < kQuadrants) runs[(int64_t)t * kQuadrants + tid] = 0;
       if (tid == 0 && flags) flags[t] = overflow ? MISA_FLAG_OVERFLOW : MISA_FLAG_UNDERFLOW;
       __syncthreads();  // pf (next row) published before anyone reads it
       continue;
@@ -1296,12 +1303,46 @@ __global__ void __launch_bounds__(NT, ((NT <= 256 || EPT <= 12) ? 2 : 1)) topk5_
       }
     }
     if (lane == 0) sh.wtot[w] = cnt;
-    for (int i = tid; i < nch; i += NT) {
-      H[i] = 0u;
-      G0[i] = 0xffffffffu;
+    if (!UO) {
+      for (int i = tid; i < nch; i += NT) {
+        H[i] = 0u;
+        G0[i] = 0xffffffffu;
+      }
     }
     __syncthreads();
     SEL_MARK(ti_, 4);
+    if constexpr (UO) {
+      // list-major compaction straight to the output row; run q = the selected keys of list q
+      int run = warps_exclusive<NW>(sh.wtot, w);
+      const uint32_t lt = ptx::lanemask_lt();
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const bool sel = (selm >> r) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+        if (sel) {
+          const int g = run + __popc(bal & lt);
+          out[g] = idx[r];
+          if (want_scores) outs[g] = key_float(key[r]);
+        }
+        run += __popc(bal);
+      }
+      if (tid < kQuadrants) {
+        int c = 0;
+        for (int i = 0; i < WPL; ++i) c += sh.wtot[tid * WPL + i];
+        runs[(int64_t)t * kQuadrants + tid] = c;
+      }
+      for (int i = kk + tid; i < k; i += NT) {
+        out[i] = -1;
+        if (outs) outs[i] = -INFINITY;
+      }
+      __syncthreads();  // wtot / hist reads done before the next row reuses them; pf published
+      if (tid == 0) {
+        launch();
+        load_meta(t + 2 * gridDim.x);
+        if (flags) flags[t] = 0;
+      }
+      continue;
+    }
     int run = warps_exclusive<NW>(sh.wtot, w);
     const uint32_t lt = ptx::lanemask_lt();
 #pragma unroll
@@ -1384,7 +1425,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
                                                        const int32_t* __restrict__ row_len,
                                                        const int32_t* __restrict__ rows, int k,
                                                        int32_t* __restrict__ topk, int64_t topk_ld,
-                                                       float* __restrict__ topk_scores) {
+                                                       float* __restrict__ topk_scores,
+                                                       const int32_t* __restrict__ runs = nullptr) {
+  // runs (optional): the row is kQuadrants consecutive ascending runs of these lengths
+  // (misa_select_topk_runs output) instead of one ascending list
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ SelSh<NT> sh;
   const int rr = rows ? rows[blockIdx.x] : blockIdx.x;
@@ -1401,7 +1445,18 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
     }
     return;
   }
-  if (threadIdx.x == 0) {
+  int NL = 1;
+  if (runs) {
+    NL = kQuadrants;
+    if (threadIdx.x == 0) {
+      int o = 0;
+      for (int q = 0; q < kQuadrants; ++q) {
+        sh.lst_off[q] = min(o, n);
+        o += runs[(int64_t)rr * kQuadrants + q];
+      }
+      sh.lst_off[kQuadrants] = n;
+    }
+  } else if (threadIdx.x == 0) {
     sh.lst_off[0] = 0;
     sh.lst_off[1] = n;
   }
@@ -1426,7 +1481,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) dense_reg_kernel(cons
       if (e < n) si[e] = ix[r];
     }
   };
-  v3_dispatch<NT, EPT>(n, load, 1, kk, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
+  v3_dispatch<NT, EPT>(n, load, NL, kk, sh, sidx, cidx, outs ? csc : nullptr, out, outs, k);
 }
 
 // Global path for rows longer than the register capacity (exact fallback): MSB radix
@@ -1981,12 +2036,12 @@ template <int NT, int EPT>
 struct DenseL {
   static int go(cudaStream_t st, const float* s, int64_t ld, const int32_t* idx, int64_t idx_ld,
                 const int32_t* row_len, const int32_t* rows, int64_t n_rows, int k, int32_t* topk, int64_t tld,
-                float* ts) {
+                float* ts, const int32_t* runs = nullptr) {
     const size_t bytes = (size_t)NT * EPT * 4 + (size_t)k * 16;
     auto kern = idx ? (ts ? dense_reg_kernel<NT, EPT, true, true> : dense_reg_kernel<NT, EPT, true, false>)
                     : (ts ? dense_reg_kernel<NT, EPT, false, true> : dense_reg_kernel<NT, EPT, false, false>);
     MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    kern<<<(unsigned)n_rows, NT, bytes, st>>>(s, ld, idx, idx_ld, row_len, rows, k, topk, tld, ts);
+    kern<<<(unsigned)n_rows, NT, bytes, st>>>(s, ld, idx, idx_ld, row_len, rows, k, topk, tld, ts, runs);
     MISA_LAUNCH_CHECK();
     return MISA_OK;
   }
@@ -2015,32 +2070,49 @@ struct ListKthL {
 // v5 selector when the quadrant capacity maps onto whole warps and the staging fits.
 template <int NT, int EPT>
 static int launch_topk5_t(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl,
-                          int64_t T, int k, int n_chunks, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
-  const size_t bytes = (size_t)kQuadrants * cap * 8 + (size_t)n_chunks * 8 + (size_t)k * (ts ? 8 : 4);
+                          int64_t T, int k, int n_chunks, int32_t* topk, int64_t ld, float* ts, int32_t* flags,
+                          int32_t* runs) {
+  // unordered (runs): no chunk histogram / compacted staging
+  const size_t bytes = (size_t)kQuadrants * cap * 8 + (runs ? 0 : (size_t)n_chunks * 8 + (size_t)k * (ts ? 8 : 4));
   if (bytes > 200 * 1024) return -100;
-  auto kern = ts ? topk5_kernel<NT, EPT, true> : topk5_kernel<NT, EPT, false>;
+  auto kern = runs ? (ts ? topk5_kernel<NT, EPT, true, true> : topk5_kernel<NT, EPT, false, true>)
+                   : (ts ? topk5_kernel<NT, EPT, true, false> : topk5_kernel<NT, EPT, false, false>);
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   int per_sm = 0;
   MISA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes));
   const int64_t grid = std::min<int64_t>(T, (int64_t)sm_count() * std::max(per_sm, 1));
-  kern<<<(unsigned)grid, NT, bytes, st>>>(cand, cc, cap, pl, (int)T, k, n_chunks, topk, ld, ts, flags);
+  kern<<<(unsigned)grid, NT, bytes, st>>>(cand, cc, cap, pl, (int)T, k, n_chunks, topk, ld, ts, flags, runs);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }
 
 static int launch_topk5(cudaStream_t st, const uint64_t* cand, const int32_t* cc, int cap, const int32_t* pl,
-                        int64_t T, int k, int64_t max_n, int32_t* topk, int64_t ld, float* ts, int32_t* flags) {
+                        int64_t T, int k, int64_t max_n, int32_t* topk, int64_t ld, float* ts, int32_t* flags,
+                        int32_t* runs = nullptr) {
   const int64_t n_chunks = (max_n + 31) / 32;
   if (n_chunks > 8192 || cap > 0xffff) return -100;
   const int nc = static_cast<int>(n_chunks);
   // NT*EPT == 4*cap with cap a multiple of 32*EPT*(NT/128)
-  if (cap == 256 * 8 / 4) return launch_topk5_t<256, 8>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
-  if (cap == 256 * 16 / 4) return launch_topk5_t<256, 16>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
-  if (cap == 512 * 12 / 4) return launch_topk5_t<512, 12>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
-  if (cap == 256 * 32 / 4) return launch_topk5_t<256, 32>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
-  if (cap == 512 * 24 / 4) return launch_topk5_t<512, 24>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
-  if (cap == 512 * 32 / 4) return launch_topk5_t<512, 32>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags);
+#define MISA_TOPK5_CASE(NT_, EPT_) \
+  if (cap == NT_ * EPT_ / 4) return launch_topk5_t<NT_, EPT_>(st, cand, cc, cap, pl, T, k, nc, topk, ld, ts, flags, runs);
+  MISA_TOPK5_CASE(256, 8)
+  MISA_TOPK5_CASE(256, 16)
+  MISA_TOPK5_CASE(512, 12)
+  MISA_TOPK5_CASE(256, 32)
+  MISA_TOPK5_CASE(512, 24)
+  MISA_TOPK5_CASE(512, 32)
+#undef MISA_TOPK5_CASE
   return -100;
+}
+
+// runs[t] = (min(k, n_t), 0, 0, 0): one ascending run (rows selected by an ordered path)
+__global__ void single_run_kernel(const int32_t* __restrict__ prefix_len, int64_t n_rows, int k,
+                                  int32_t* __restrict__ runs) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n_rows) {
+    const int n = prefix_len[t];
+    *reinterpret_cast<int4*>(runs + 4 * t) = make_int4(n < k ? (n > 0 ? n : 0) : k, 0, 0, 0);
+  }
 }
 }  // namespace
 
@@ -2077,6 +2149,26 @@ extern "C" int misa_select_topk(const uint64_t* cand, const int32_t* cand_count,
                                   n_rows, k, topk, topk_ld, topk_scores, flags);
 }
 
+extern "C" int misa_select_topk_runs(const uint64_t* cand, const int32_t* cand_count, int cap,
+                                     const int32_t* prefix_len, int64_t n_rows, int k, int64_t max_prefix_len,
+                                     int32_t* topk, int64_t topk_ld, int32_t* runs, int32_t* flags, void* stream) {
+  MISA_REQUIRE(cand && cand_count && prefix_len && topk && runs, "null pointer");
+  MISA_REQUIRE(k >= 1 && cap >= 1 && topk_ld >= k && n_rows >= 1, "bad top-k arguments");
+  MISA_REQUIRE((reinterpret_cast<uintptr_t>(runs) & 15) == 0, "runs must be 16-byte aligned");
+  if (max_prefix_len > 0) {
+    const int rc = launch_topk5(as_stream(stream), cand, cand_count, cap, prefix_len, n_rows, k, max_prefix_len, topk,
+                                topk_ld, nullptr, flags, runs);
+    if (rc != -100) return rc;
+  }
+  // no unordered kernel for this capacity: the ascending selection is one run
+  const int rc = misa_select_topk(cand, cand_count, cap, prefix_len, n_rows, k, max_prefix_len, topk, topk_ld,
+                                  nullptr, flags, stream);
+  if (rc) return rc;
+  single_run_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, as_stream(stream)>>>(prefix_len, n_rows, k, runs);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}
+
 extern "C" int misa_select_dense(const float* scores, int64_t ld, const int32_t* idx, int64_t idx_ld,
                                  const int32_t* row_len, const int32_t* rows, int64_t n_rows, int k, int32_t* topk,
                                  int64_t topk_ld, float* topk_scores, void* stream) {
@@ -2092,6 +2184,19 @@ extern "C" int misa_select_dense(const float* scores, int64_t ld, const int32_t*
                                                                  topk_ld, topk_scores);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
+}
+
+extern "C" int misa_select_dense_runs(const float* scores, int64_t ld, const int32_t* idx, int64_t idx_ld,
+                                      const int32_t* row_len, const int32_t* runs, int64_t n_rows, int k,
+                                      int32_t* topk, int64_t topk_ld, void* stream) {
+  MISA_REQUIRE(scores && idx && row_len && runs && topk, "null pointer");
+  MISA_REQUIRE(k >= 1 && topk_ld >= k, "bad k");
+  MISA_REQUIRE((size_t)k * 16 <= 200 * 1024, "k too large");
+  if (n_rows <= 0) return MISA_OK;
+  const int rc = dispatch_capacity<DenseL>(ld, as_stream(stream), scores, ld, idx, idx_ld, row_len, nullptr, n_rows,
+                                           k, topk, topk_ld, nullptr, runs);
+  MISA_REQUIRE(rc != -100, "row length %lld exceeds the register selector", (long long)ld);
+  return rc;
 }
 
 extern "C" int misa_merge_topk(const float* part_scores, const int32_t* part_idx, int n_parts, int64_t part_stride,

@@ -72,8 +72,21 @@ class IndexerOutput:
     topk: torch.Tensor                  # (T, k) int32, ascending, -1 padded
     heads: torch.Tensor | None = None   # (T, h) int32 ascending (misa / misa_hier)
     importance: torch.Tensor | None = None  # (T, H) f32 router importance
-    candidates: torch.Tensor | None = None  # (T, k') int32 coarse candidates (misa_hier)
+    candidates: torch.Tensor | None = None  # (T, k') int32 coarse candidates (misa_hier), -1 padded
     n_fallback_rows: int = 0
+    # (T, 4) int32: when set, row t of `candidates` is 4 consecutive ascending runs of these
+    # lengths (the coarse selector's unordered output); None: each row is ascending
+    candidate_runs: torch.Tensor | None = None
+
+    def sorted_candidates(self) -> torch.Tensor | None:
+        """The coarse candidates ascending per row (-1 padding last), as ``topk_tokens``
+        returns them (``routing.py:157-159``)."""
+        if self.candidates is None or self.candidate_runs is None:
+            return self.candidates
+        c = self.candidates.long()
+        c = torch.where(c < 0, torch.iinfo(torch.int64).max, c)
+        c = torch.sort(c, dim=1).values
+        return torch.where(c == torch.iinfo(torch.int64).max, -1, c).to(torch.int32)
 
 
 @dataclass
@@ -417,8 +430,8 @@ class IndexerEngine:
         """
         if k < 4096:
             stride, beta = self.stride, (self.beta or 2.0)
-        else:
-            stride, beta = max(1, self.stride // 2), (self.beta or 1.3)
+        else:  # j >= 600 samples: a 4 % spread, so beta = 1.2 is still > 5 sigma from underflow
+            stride, beta = max(1, self.stride // 2), (self.beta or 1.2)
         stride = max(stride, -(-L // 16384))  # <= 16384 samples per row bounds the (T, L/stride) sample buffer
         j = max(1.0, beta * k / stride)
         cap = int(math.ceil((1.0 + 5.5 / math.sqrt(j)) * beta * k / 4 / 32)) * 32
@@ -490,11 +503,13 @@ class IndexerEngine:
         return heads, hq, imp
 
     def select(self, x: PreparedInputs, heads: torch.Tensor | None, hq: int, k: int, out: torch.Tensor,
-               tag: str = "sel", scores: torch.Tensor | None = None) -> int:
+               tag: str = "sel", scores: torch.Tensor | None = None, runs: torch.Tensor | None = None) -> int:
         """Fused streaming top-k over the given head set (None = all heads). Returns #fallback rows.
 
         With ``scores`` (T, k) f32 the selected scores are returned too (aligned with ``out``)
-        and short rows are scored rather than short-cut — what a key shard's local top-k needs."""
+        and short rows are scored rather than short-cut — what a key shard's local top-k needs.
+        With ``runs`` (T, 4) int32 the rows are left unordered: 4 ascending runs of these
+        lengths (``misa_select_topk_runs``)."""
         dev = x.keys.device
         stride, beta, cap = self.selector_params(k, x.L)
         append_all = 4 * cap
@@ -546,9 +561,13 @@ class IndexerEngine:
         flags = self._buf(tag + "_flags", (x.T,), torch.int32, dev)
         self.last_flags = flags
         self._mark(tag + ":select")
-        _lib.call("misa_select_topk", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, x.L, _ptr(out),
-                  out.stride(0),
-                  _ptr(scores), _ptr(flags), stream)
+        if runs is not None and scores is None:
+            _lib.call("misa_select_topk_runs", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, x.L, _ptr(out),
+                      out.stride(0), _ptr(runs), _ptr(flags), stream)
+        else:
+            runs = None
+            _lib.call("misa_select_topk", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, x.L, _ptr(out),
+                      out.stride(0), _ptr(scores), _ptr(flags), stream)
         self._mark(tag + ":end")
         if not self.check_overflow:
             return 0
@@ -556,6 +575,9 @@ class IndexerEngine:
         if bad.numel() == 0:
             return 0
         self._dense_rows(x, heads, hq, k, out, bad.cpu().numpy(), scores)
+        if runs is not None:  # re-selected rows are ascending: one run
+            runs[bad] = 0
+            runs[bad, 0] = torch.clamp_max(x.prefix[bad], k)
         return int(bad.numel())
 
     def _dense_rows(self, x: PreparedInputs, heads, hq, k, out, rows: np.ndarray, scores=None):
@@ -586,8 +608,10 @@ class IndexerEngine:
         if scores is not None:
             scores[sel] = so
 
-    def refine(self, x: PreparedInputs, cand: torch.Tensor, k: int, out: torch.Tensor):
-        """K5 + dense select within candidates (MISA-dagger fine stage)."""
+    def refine(self, x: PreparedInputs, cand: torch.Tensor, k: int, out: torch.Tensor,
+               runs: torch.Tensor | None = None):
+        """K5 + dense select within candidates (MISA-dagger fine stage); ``runs``: the
+        candidates are the coarse selector's 4 ascending runs per row."""
         dev = x.keys.device
         kp = cand.shape[1]
         ckey = x.list_key()
@@ -605,8 +629,12 @@ class IndexerEngine:
                   _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(rows), rows.numel(), x.T,
                   None if x.seq is None else _ptr(x.seq.key0), _ptr(rs), kp, stream)
         self._mark("refine_select")
-        _lib.call("misa_select_dense", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), None, x.T, k,
-                  _ptr(out), out.stride(0), None, stream)
+        if runs is not None:
+            _lib.call("misa_select_dense_runs", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(runs),
+                      x.T, k, _ptr(out), out.stride(0), stream)
+        else:
+            _lib.call("misa_select_dense", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), None, x.T, k,
+                      _ptr(out), out.stride(0), None, stream)
         self._mark("refine:end")
 
     # ----------------------------------------------------------- decode
@@ -865,7 +893,7 @@ class IndexerEngine:
             nfb += r.n_fallback_rows
             if flags is not None:
                 flags[a:b].copy_(self.last_flags[: b - a])
-            for name in ("heads", "importance", "candidates"):
+            for name in ("heads", "importance", "candidates", "candidate_runs"):
                 v = getattr(r, name)
                 if v is None:
                     continue
@@ -894,11 +922,12 @@ class IndexerEngine:
                                  n_fallback_rows=nfb)
         kp = max(self.kprime, k)
         cand = self._buf("hier_cand", (x.T, kp), torch.int32, dev)
-        nfb = self.select(x, heads, hq, kp, cand, tag="coarse")
-        self.refine(x, cand, k, out)
+        runs = self._buf("hier_runs", (x.T, 4), torch.int32, dev)
+        nfb = self.select(x, heads, hq, kp, cand, tag="coarse", runs=runs)
+        self.refine(x, cand, k, out, runs=runs)
         self.last_fallback_rows = nfb
         return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H],
-                             candidates=cand, n_fallback_rows=nfb)
+                             candidates=cand, n_fallback_rows=nfb, candidate_runs=runs)
 
 
 _SHARED: dict = {}

@@ -108,7 +108,7 @@ def misa_hier_select(workload: IndexerWorkload, summary: BlockSummary, cfg: Inde
     heads = res.heads[0].cpu().numpy()
     hs = HeadSet(heads[heads >= 0].astype(np.int64), workload.n_heads)
     c = res.candidates[0].cpu().numpy()
-    cand = TokenSelection(c[c >= 0].astype(np.int64), cfg.candidate_kprime, workload.prefix_len)
+    cand = TokenSelection(np.sort(c[c >= 0]).astype(np.int64), cfg.candidate_kprime, workload.prefix_len)
     o = res.topk[0].cpu().numpy()
     sel = TokenSelection(o[o >= 0].astype(np.int64), cfg.budget_k, workload.prefix_len)
     ledger = _ledger(workload, summary.n_blocks, len(hs), kind, refine=workload.n_heads * len(cand))

@@ -44,7 +44,7 @@ def c4():
         if r.importance is not None:
             keep["importance"] = r.importance.clone()
         if r.candidates is not None:
-            keep["candidates"] = r.candidates.clone()
+            keep["candidates"] = r.sorted_candidates().clone()
         out[method] = keep
         fallback[method] = eng.last_fallback_rows
         del eng
@@ -145,16 +145,19 @@ def _pack(scores_row: np.ndarray, keys: np.ndarray, cap: int):
     return lists, cnt
 
 
-@pytest.mark.parametrize("with_scores", [False, True])
-def test_coarse_selector_kprime_8192_cap_4096(with_scores):
-    """misa_select_topk at the MISA-dagger C4 coarse shape (k = 8192, cap 4096 per quadrant:
-    the topk5<512,32> kernel), rows of up to 131072 keys with forced ties and -0/+0,
-    against a (score desc, index asc) sort; under/overflowing rows are flagged."""
+@pytest.mark.parametrize("cap,mode", [(4096, "ordered"), (4096, "scores"), (3072, "ordered"), (3072, "runs")])
+def test_coarse_selector_kprime_8192(cap, mode):
+    """misa_select_topk at the MISA-dagger C4 coarse shape (k = 8192; cap 3072 per quadrant is
+    the engine's choice at beta = 1.2, topk5<512,24>; 4096 is topk5<512,32>), rows of up to
+    131072 keys with forced ties and -0/+0, against a (score desc, index asc) sort;
+    under/overflowing rows are flagged.  mode "runs": the unordered variant
+    (misa_select_topk_runs) must give the same set as 4 ascending runs, and the re-rank
+    selector over those runs (misa_select_dense_runs) the same top-k as over the sorted set."""
     from paper_2605_07363_b200 import _lib
     from paper_2605_07363_b200.engine import IndexerEngine
     k = 8192
-    _, _, cap = IndexerEngine("misa", budget_k=2048).selector_params(k, L)
-    assert cap == 4096
+    _, _, eng_cap = IndexerEngine("misa", budget_k=2048).selector_params(k, L)
+    assert eng_cap == 3072
     rng = np.random.default_rng(7)
     R = 320  # > 2 rows per SM: the persistent kernel's prefetch ring wraps
     n_rows = rng.integers(20000, L + 1, R)
@@ -169,7 +172,7 @@ def test_coarse_selector_kprime_8192_cap_4096(with_scores):
             s = np.round(s * 8) / 8  # heavy ties: the index tie-break decides
         s[rng.integers(0, n, 50)] = -0.0
         s[rng.integers(0, n, 50)] = 0.0
-        target = 12000 if r != 1 else 6000  # row 1 underflows (< k candidates of n >= k keys)
+        target = int(2.9 * cap) if r != 1 else 6000  # row 1 underflows (< k candidates of n >= k keys)
         if r == 2:
             target = n  # row 2: every one of its 9000 keys is a candidate
         tau = np.sort(s)[::-1][min(target, n) - 1]
@@ -184,20 +187,55 @@ def test_coarse_selector_kprime_8192_cap_4096(with_scores):
     cd = torch.from_numpy(cand.view(np.int64).reshape(-1)).cuda()
     cc = torch.from_numpy(cnt.reshape(-1)).cuda()
     out = torch.empty(R, k, dtype=torch.int32, device="cuda")
-    sc = torch.empty(R, k, device="cuda") if with_scores else None
+    sc = torch.empty(R, k, device="cuda") if mode == "scores" else None
     flags = torch.zeros(R, dtype=torch.int32, device="cuda")
-    _lib.call("misa_select_topk", cd.data_ptr(), cc.data_ptr(), cap, prefix.data_ptr(), R, k, L, out.data_ptr(), k,
-              None if sc is None else sc.data_ptr(), flags.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    stream = torch.cuda.current_stream().cuda_stream
+    runs = torch.empty(R, 4, dtype=torch.int32, device="cuda")
+    if mode == "runs":
+        _lib.call("misa_select_topk_runs", cd.data_ptr(), cc.data_ptr(), cap, prefix.data_ptr(), R, k, L,
+                  out.data_ptr(), k, runs.data_ptr(), flags.data_ptr(), stream)
+    else:
+        _lib.call("misa_select_topk", cd.data_ptr(), cc.data_ptr(), cap, prefix.data_ptr(), R, k, L, out.data_ptr(),
+                  k, None if sc is None else sc.data_ptr(), flags.data_ptr(), stream)
     torch.cuda.synchronize()
     fl = flags.cpu().numpy()
     got = out.cpu().numpy()
+    rn = runs.cpu().numpy()
     assert fl[1] != 0 and fl[3] != 0
     for r in range(R):
         if r in (1, 3):
             continue
         assert fl[r] == 0, r
         exp, s = expect[r]
-        assert got[r, : len(exp)].tolist() == exp, r
+        row = got[r, : len(exp)]
+        if mode == "runs":
+            assert rn[r].sum() == len(exp), r
+            o = np.concatenate([[0], np.cumsum(rn[r])])
+            for q in range(4):
+                assert np.all(np.diff(row[o[q]:o[q + 1]]) > 0), (r, q)
+            assert sorted(row.tolist()) == exp, r
+        else:
+            assert row.tolist() == exp, r
         assert (got[r, len(exp):] == -1).all()
         if sc is not None:
             np.testing.assert_array_equal(sc[r, : len(exp)].cpu().numpy(), s[exp])
+    if mode != "runs":
+        return
+    # re-rank selection over the runs == over the ascending set (fine scores: fresh, tied)
+    ok = np.array([r not in (1, 3) for r in range(R)])
+    rows = torch.from_numpy(np.nonzero(ok)[0]).cuda()
+    ci = out[rows].contiguous()
+    nc = (ci >= 0).sum(1).to(torch.int32)
+    fine = torch.round(torch.randn(ci.shape, device="cuda") * 4) / 4
+    fine[ci < 0] = 0
+    kf = 2048
+    o1 = torch.empty(rows.numel(), kf, dtype=torch.int32, device="cuda")
+    _lib.call("misa_select_dense_runs", fine.data_ptr(), k, ci.data_ptr(), k, nc.data_ptr(),
+              runs[rows].contiguous().data_ptr(), rows.numel(), kf, o1.data_ptr(), kf, stream)
+    torch.cuda.synchronize()
+    f = fine.cpu().numpy()
+    c = ci.cpu().numpy()
+    for i in range(rows.numel()):
+        m = c[i] >= 0
+        order = sorted(range(int(m.sum())), key=lambda j: (-float(f[i, j]), int(c[i, j])))[:kf]
+        assert o1[i].cpu().numpy()[: len(order)].tolist() == sorted(c[i, order].tolist()), i

@@ -123,7 +123,7 @@ def test_golden_prefill_parity(golden_dir, name):
         hm = np.abs(ws[gh]) @ np.abs(qs[gh] @ keys.T)
         check_topk(r_m.topk[t].cpu().numpy(), ms, hm, m["k"], cm, f"{name} misa t={t}")
         # MISA-dagger: coarse candidates (routed) then all-head re-rank inside them
-        cand = r_h.candidates[t].cpu().numpy()
+        cand = r_h.sorted_candidates()[t].cpu().numpy()
         check_topk(cand, ms, hm, max(m["kp"], m["k"]), ch, f"{name} hier-coarse t={t}")
         cand = cand[cand >= 0]
         fine = O.gated_relu_scores(keys[cand], qs, ws, "fast32")
@@ -200,7 +200,7 @@ def test_hier_containment_and_nesting():
     pools = []
     for kp in (100, 200, 400, 2500):
         r_h, _ = _run("misa_hier", K, Q, W, budget_k=100, active_heads_h=2, block_size=128, candidate_kprime=kp)
-        cand = r_h.candidates.cpu().numpy()
+        cand = r_h.sorted_candidates().cpu().numpy()
         sel = r_h.topk.cpu().numpy()
         dense = r_d.topk.cpu().numpy()
         for t in range(0, 2500, 37):

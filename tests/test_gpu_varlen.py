@@ -82,6 +82,6 @@ def test_varlen_explicit_prefixes_match_oracle():
         ms = O.misa_score(keys, qs, ws, gh, "fast32")
         hm = np.abs(ws[gh]) @ np.abs(qs[gh] @ keys.T)
         check_topk(out["misa"].topk[t].cpu().numpy(), ms, hm, k, cm, f"misa t={t}")
-        check_topk(out["misa_hier"].candidates[t].cpu().numpy(), ms, hm, 4096, ch, f"hier coarse t={t}")
+        check_topk(out["misa_hier"].sorted_candidates()[t].cpu().numpy(), ms, hm, 4096, ch, f"hier coarse t={t}")
     for c in (cd, cm, ch):
         assert c.recall() >= 0.999, c.recall()

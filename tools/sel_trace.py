@@ -23,7 +23,7 @@ K = torch.randn(L, 128, device="cuda", generator=g).bfloat16()
 Q = torch.randn(L, 64, 128, device="cuda", generator=g).bfloat16()
 W = torch.softmax(torch.randn(L, 64, device="cuda", generator=g), -1).float()
 x = prepare_inputs(K, Q, W)
-eng = IndexerEngine("misa")
+eng = IndexerEngine(os.environ.get("METHOD", "misa"), beta=float(os.environ["BETA"]) if "BETA" in os.environ else None)
 eng.run_prepared(x); eng.run_prepared(x)
 torch.cuda.synchronize()
 lib = _lib.load()
