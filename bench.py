@@ -70,6 +70,13 @@ def _workload_name(a):
     return f"C4 causal prefill L=T={a.L} H={a.H} h={a.h} d={a.d} B={a.B} k={a.k}"
 
 
+def _config(a, world):
+    """The workload config, identical in both arms (ours / --impl reference)."""
+    return {"workload": _workload_name(a), "L": a.L, "T": a.L, "H": a.H, "h": a.h, "d": a.d, "B": a.B, "k": a.k,
+            "parallelism": f"key-sharded x{world}" if world > 1 else "single device",
+            "l2": "inputs larger than L2 (queries 2 GiB); no explicit flush"}
+
+
 def _peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -159,12 +166,15 @@ def run_reference(a):
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "ms/layer", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": v, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (fast32)", "data": "synthetic",
-            "config": {"workload": _workload_name(a), "L": a.L, "T": a.L, "H": a.H, "h": a.h, "d": a.d,
-                       "B": a.B, "k": a.k},
-            "cpu_baseline": {"value": v, "unit": "ms/layer", "cores": cores, "kind": "port",
+            "config": _config(a, int(os.environ.get("WORLD_SIZE", "1"))),
+            "value_is_extrapolated": True,
+            "cpu_baseline": {"value": v, "unit": "ms/layer", "cores": cores, "cpu_model": cpu_bench.cpu_model(),
+                             "kind": "port",
                              "sample": f"{info['rows']} stratified causal rows per step, per-row reference "
                                        f"misa select (pool+route+score+top-k, fast32), extrapolated "
-                                       f"linearly in prefix length over all {a.L} rows / {cores} cores"},
+                                       f"linearly in prefix length over all {a.L} rows / {cores} cores: a full "
+                                       f"layer on the CPU would not fit the driver's run, so each step is a "
+                                       f"bounded sample and the value is an extrapolation"},
             "e2e": {"value": v, "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -452,11 +462,31 @@ def run_ours(a):
     if filt_ms:
         ach = flops_misa / (filt_ms * 1e-3) / 1e12
         roof = {"kernel": "score_kernel<128,8,FILTER> (MISA routed-head scoring + fused top-k filter)",
-                "bound": "tensor", "achieved": round(ach, 1), "peak": tc_sust, "unit": "TFLOP/s",
-                "frac": round(ach / tc_sust, 4), "traffic": traffic,
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a multi-kernel step)",
+                "bound": "tensor", "achieved": round(ach, 1), "peak": tc_burst, "unit": "TFLOP/s",
+                "frac": round(ach / tc_burst, 4), "frac_vs_sustained_peak": round(ach / tc_sust, 4),
+                "traffic": traffic,
+                "peak_source": f"{peak_src} bf16_tflops (burst; the sustained figure was measured at a lower "
+                               f"clock than this run's, so it is reported beside it, not as the bound)",
                 "flops_per_launch": flops_misa, "launch_ms": round(filt_ms, 3)}
-    layer_frac = flops_misa / (misa_ms * 1e-3) / 1e12 / tc_sust
+    layer_frac = flops_misa / (misa_ms * 1e-3) / 1e12 / tc_burst
+    # per-kernel roofline fractions of the MISA layer (SURVEY.md §8(d) algorithmic work)
+    kernel_fracs = {}
+    if stages:
+        D, Hp = (64 if a.d <= 64 else 128), max(8, 1 << (a.H - 1).bit_length())
+        hq = max(8, 1 << (a.h - 1).bit_length())
+        stride = 32
+        def hb(name, nbytes):
+            ms = stages.get(name)
+            if ms:
+                kernel_fracs[name] = {"bound": "hbm", "bytes": int(nbytes), "GB_s": round(nbytes / ms / 1e6, 1),
+                                      "frac": round(nbytes / ms / 1e6 / hbm, 4)}
+        hb("route_scores", T * Hp * D * 2 + T * Hp * 4)
+        hb("route_select", T * Hp * 4 * 2 + T * hq * 4)
+        hb("sel:threshold", T * ((L + stride - 1) // stride) * 4 // 2)
+        hb("sel:sample", T * hq * D * 2 + L * D * 2)
+        hb("sel:select", T * a.k * 4)
+        if filt_ms:
+            kernel_fracs["sel:filter"] = {"bound": "tensor", "TFLOP_s": round(ach, 1), "frac": round(ach / tc_burst, 4)}
 
     cpu = None
     if not a.no_cpu and world == 1:
@@ -466,7 +496,8 @@ def run_ours(a):
         Qs = Q[torch.as_tensor(srows)].double().cpu().numpy()
         Ws = W[torch.as_tensor(srows)].double().cpu().numpy()
         info = cpu_bench.time_layer("misa", Kn, Qs, Ws, srows, L, T, k=a.k, h=a.h, B=a.B, kp=a.kprime, cores=cores)
-        cpu = {"value": round(info["ms_per_layer"], 1), "unit": "ms/layer", "cores": cores, "kind": "port",
+        cpu = {"value": round(info["ms_per_layer"], 1), "unit": "ms/layer", "cores": cores,
+               "cpu_model": cpu_bench.cpu_model(), "kind": "port",
                "sample": f"{info['rows']} stratified causal rows of this workload, per-row reference misa select "
                          f"(pool+route+score+top-k, fast32) in {cores} single-BLAS-thread processes "
                          f"({info['cpu_s']:.1f} s CPU), extrapolated linearly in prefix length to all {T} rows"}
@@ -496,13 +527,13 @@ def run_ours(a):
         "warmup": a.warmup, "ms_per_step": round(misa_ms, 3), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (torch randn keys/queries, softmax gates, seed 0)",
-        "config": {"workload": _workload_name(a), "L": L, "T": T, "H": a.H, "h": a.h, "d": a.d, "B": a.B,
-                   "k": a.k, "parallelism": f"key-sharded x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (queries 2 GiB); no explicit flush"},
+        "config": _config(a, world),
         "dsa_ms_per_layer": round(dsa_ms, 3), "speedup_vs_dsa": round(dsa_ms / misa_ms, 3),
         "topk_recall_vs_cpu_reference": round(recall, 6), "topk_recall_by_method": recall_by, "recall_rows": rows,
         "misa_iou_vs_dsa_random_data": round(float(np.mean(iou)), 4),
         "scores_per_s": P / (misa_ms * 1e-3), "layer_tensor_frac": round(layer_frac, 4),
+        "layer_tensor_frac_note": "MISA FLOPs / layer time / burst bf16 peak",
+        "kernel_fracs": kernel_fracs,
         "misa_stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "dsa_stages_ms": {k: round(v, 4) for k, v in dstages.items()},
         "fallback_rows": fallback,
@@ -511,7 +542,19 @@ def run_ours(a):
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)
+        line["misa_hier_speedup_vs_dsa"] = round(dsa_ms / hier_ms, 3)
         line["misa_hier_stages_ms"] = {k: round(v, 4) for k, v in hstages.items()}
+        rms = hstages.get("refine")
+        if rms:
+            n_ref = float(np.minimum(np.arange(1, T + 1, dtype=np.float64), a.kprime).sum())
+            fl = 2.0 * a.H * a.d * n_ref
+            gb = n_ref * (64 if a.d <= 64 else 128) * 2
+            line["misa_hier_refine_roofline"] = {
+                "kernel": "refine_kernel (all-head re-score of the gathered k' candidates)",
+                "TFLOP_s": round(fl / rms / 1e9, 1), "frac_tensor_burst": round(fl / rms / 1e9 / tc_burst, 4),
+                "gather_TB_s": round(gb / rms / 1e9, 2),
+                "gather_note": "candidate key rows gathered from the L2-resident key set; tools/ubench_gather.cu "
+                               "measured 15.7 TB/s for the same cp.async gather with nothing else running"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -32,6 +32,7 @@
  *   misa_select_dense     dsa.py:64-92       topk_tokens / topk_within over a dense score row
  *   misa_select_dense_long dsa.py:64-76      topk_tokens over long dense rows (decode), all SMs
  *   misa_refine_scores    dsa.py:95-115      dsa_rescore (MISA-dagger fine stage), routing.py:144-174
+ *   misa_refine_candidates dsa.py:95-115     the same, scores packed as misa_select_topk candidate lists
  *   misa_merge_topk       (no reference counterpart: key-sharded multi-GPU merge)
  *   misa_shard_map_indices (no reference counterpart: local -> global key index of a shard)
  *   misa_list_kth / misa_list_prune (no reference counterpart: pruned key-shard exchange)
@@ -234,6 +235,18 @@ int misa_relevance_dots(const void* keys, int64_t n_keys, int head_dim, const vo
  * counts elements bf16 does not represent exactly. */
 int misa_pack_rows_f64(const double* src, int64_t n_rows, int d, int64_t group, int64_t dst_group_stride, void* dst,
                        int D, int64_t dst_row0, unsigned long long* n_inexact, void* stream);
+
+/* misa_refine_scores with the scores packed for misa_select_topk: lists[t][i] = cand[t][i] << 32 |
+ * f32 bits of the score, i < n_cand[t] <= 4 * list_cap, viewed as 4 lists of list_cap slots
+ * (list_count[t][q] = the filled slots of list q).  When cand holds a coarse selection whose
+ * 32-key chunks are contiguous (misa_select_topk / _runs output), misa_select_topk over these
+ * lists with prefix_len = the rows' prefix lengths is the re-rank's top-k (dsa.py:79-92), the
+ * ascending order coming from its chunk scan. */
+int misa_refine_candidates(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                           const float* weights, int n_heads, int n_heads_pad, const int32_t* cand, int64_t cand_ld,
+                           const int32_t* n_cand, const int32_t* rows, int n_items, int64_t n_rows,
+                           const int32_t* row_key0, uint64_t* lists, int list_cap, int32_t* list_count,
+                           void* stream);
 
 /* Multi-GPU merge: n_parts local (score, index) top-k lists per row (parts[p][t][i], scores
  * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc).

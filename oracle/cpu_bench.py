@@ -42,8 +42,20 @@ def _row(args):
 def sample_rows(L: int, T: int, count: int) -> np.ndarray:
     """Stratified rows over the causal range: first, last, block-boundary-ish and evenly spaced."""
     first = L - T
-    rows = np.unique(np.linspace(0, T - 1, count).round().astype(np.int64))
-    return rows + 0 * first
+    return np.unique(np.linspace(0, T - 1, count).round().astype(np.int64))
+
+
+def cpu_model() -> str:
+    """The host CPU's model name (state the core count and the CPU model)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def time_layer(method: str, K: np.ndarray, Q_rows: np.ndarray, W_rows: np.ndarray, rows: np.ndarray, L: int,

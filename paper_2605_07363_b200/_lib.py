@@ -59,6 +59,8 @@ SIGNATURES: dict[str, list] = {
     "misa_shard_map_indices": [_vp, _i64, _i32, _i32, _i32, _vp],
     "misa_select_topk_runs": [_vp, _vp, _i32, _vp, _i64, _i32, _i64, _vp, _i64, _vp, _vp, _vp],
     "misa_select_dense_runs": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _vp],
+    "misa_refine_candidates": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i64, _vp, _vp, _i32, _i64, _vp, _vp,
+                               _i32, _vp, _vp],
     "misa_relevance_dots": [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _i64, _vp],
     "misa_pack_rows_f64": [_vp, _i64, _i32, _i64, _i64, _vp, _i32, _i64, _vp, _vp],
 }

@@ -37,9 +37,17 @@ struct RefineArgs {
   float* out;
   int64_t out_ld;
   int dots_tiles;  // DOTS mode: 128-key tiles per work item (item i covers keys from i * 128 * dots_tiles)
+  // packed output (misa_refine_candidates): out64[t][i] = cand[t][i] << 32 | score bits — the
+  // 4-list candidate layout of misa_select_topk (list q = positions [q*list_cap, (q+1)*list_cap))
+  uint64_t* out64;
+  int32_t* list_count;  // [T][4]
+  int list_cap;
 };
 
-constexpr int kRefGroups = 6;                            // independent producer groups
+#ifndef MISA_REF_GROUPS
+#define MISA_REF_GROUPS 6
+#endif
+constexpr int kRefGroups = MISA_REF_GROUPS;              // independent producer groups
 constexpr int kRefGroupWarps = 2;                        // warps per group (64 tile rows each)
 constexpr int kRefProd = kRefGroups * kRefGroupWarps;    // cp.async producer warps
 constexpr int kRefAcc = 4;                               // TMEM accumulators (ring)
@@ -71,6 +79,10 @@ struct RefineCfg {
                                    : (kRefAcc * N <= 256) ? 256 : 512;
   static_assert(kRefAcc * N <= 512, "TMEM accumulator ring");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
+  // a producer group never waits on a stage more than one ring round ahead of the MMA
+  // (parity waits cannot tell rounds r and r + 2 apart) when there are no more groups than
+  // stages: configurations with fewer stages (large N) leave the extra groups idle
+  static constexpr int GROUPS = kRefGroups < STAGES ? kRefGroups : STAGES;
 };
 
 // 16-byte async global->shared copy; src_bytes = 0 zero-fills the destination.
@@ -145,6 +157,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
   };
 
   if (warp < kRefProd) {
+    if (warp / kRefGroupWarps < C::GROUPS) {  // groups past C::GROUPS stay idle
     // ---------------------------------------------------------------- producers
     // group grp fills the CTA-global tiles g == grp (mod G).  Warp wi of the group covers
     // tile rows [64 wi, 64 wi + 64): instruction i moves rows 64 wi + 2i and 2i + 1
@@ -193,7 +206,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
         const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
         const __nv_bfloat16* kcur = keys;
         // next tile of this group (prefetch its indices before issuing this one)
-        j += kRefGroups;
+        j += C::GROUPS;
         const bool more = enter();
         int nxt[2] = {-1, -1};
         if (more) load_idx(j, nc, cr, nxt);
@@ -212,6 +225,7 @@ __global__ void __launch_bounds__(kRefThreads, 1)
         cur[0] = nxt[0];
         cur[1] = nxt[1];
       }
+    }
     }
   } else if (warp == kRefMma) {
     // ---------------------------------------------------------------- MMA issuer
@@ -344,7 +358,19 @@ __global__ void __launch_bounds__(kRefThreads, 1)
           }
           const float sc = gate_relu_finish(s0, s1);
           const int i = j * 128 + quad * 32 + lane;
-          if (i < nc) __stcs(a.out + (int64_t)t * a.out_ld + i, sc);  // streaming: keep L2 for the keys
+          if (a.out64) {
+            if (i < nc) {
+              const uint32_t key = static_cast<uint32_t>(__ldg(a.cand + (int64_t)t * a.cand_ld + i));
+              __stcs(reinterpret_cast<unsigned long long*>(a.out64 + (int64_t)t * a.out_ld + i),
+                     (static_cast<unsigned long long>(key) << 32) | __float_as_uint(sc));
+            }
+            if (j == 0 && quad == 0 && lane < 4) {
+              const int c = nc - lane * a.list_cap;
+              a.list_count[(int64_t)t * 4 + lane] = c < 0 ? 0 : (c > a.list_cap ? a.list_cap : c);
+            }
+          } else if (i < nc) {
+            __stcs(a.out + (int64_t)t * a.out_ld + i, sc);  // streaming: keep L2 for the keys
+          }
         }
       }
       __syncwarp();
@@ -377,12 +403,12 @@ static int launch_refine_t(const CUtensorMap& mq, const RefineArgs& a, cudaStrea
 
 using namespace misa;
 
-extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const void* queries,
-                                  const float* weights, int n_heads, int n_heads_pad, const int32_t* cand,
-                                  int64_t cand_ld, const int32_t* n_cand, const int32_t* rows, int n_items,
-                                  int64_t n_rows, const int32_t* row_key0, float* out, int64_t out_ld,
-                                  void* stream) {
-  MISA_REQUIRE(keys && queries && weights && cand && n_cand && out && (rows || n_items == 0), "null pointer");
+static int refine_launch(const void* keys, int64_t n_keys, int head_dim, const void* queries, const float* weights,
+                         int n_heads, int n_heads_pad, const int32_t* cand, int64_t cand_ld, const int32_t* n_cand,
+                         const int32_t* rows, int n_items, int64_t n_rows, const int32_t* row_key0, float* out,
+                         uint64_t* out64, int32_t* list_count, int64_t out_ld, void* stream) {
+  MISA_REQUIRE(keys && queries && weights && cand && n_cand && (out || (out64 && list_count)) && (rows || n_items == 0),
+               "null pointer");
   MISA_REQUIRE(head_dim == 64 || head_dim == 128, "head_dim must be padded to 64 or 128");
   MISA_REQUIRE(n_heads >= 1 && n_heads <= n_heads_pad && n_heads_pad <= 128, "bad head counts");
   MISA_REQUIRE(n_rows >= 1 && n_keys >= 1, "empty input");
@@ -410,6 +436,9 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
   a.H = n_heads;
   a.Hp = n_heads_pad;
   a.out = out;
+  a.out64 = out64;
+  a.list_count = list_count;
+  a.list_cap = (int)(out_ld / 4);
   a.out_ld = out_ld;
   cudaStream_t st = as_stream(stream);
   const int N = n_heads_pad < 16 ? 16 : n_heads_pad;
@@ -426,6 +455,28 @@ extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim
 #undef MISA_REFINE_CASE
   set_error("unsupported refine shape head_dim=%d heads=%d", head_dim, N);
   return MISA_EUNSUPPORTED;
+}
+
+extern "C" int misa_refine_scores(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                                  const float* weights, int n_heads, int n_heads_pad, const int32_t* cand,
+                                  int64_t cand_ld, const int32_t* n_cand, const int32_t* rows, int n_items,
+                                  int64_t n_rows, const int32_t* row_key0, float* out, int64_t out_ld,
+                                  void* stream) {
+  MISA_REQUIRE(out, "null pointer");
+  return refine_launch(keys, n_keys, head_dim, queries, weights, n_heads, n_heads_pad, cand, cand_ld, n_cand, rows,
+                       n_items, n_rows, row_key0, out, nullptr, nullptr, out_ld, stream);
+}
+
+extern "C" int misa_refine_candidates(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                                      const float* weights, int n_heads, int n_heads_pad, const int32_t* cand,
+                                      int64_t cand_ld, const int32_t* n_cand, const int32_t* rows, int n_items,
+                                      int64_t n_rows, const int32_t* row_key0, uint64_t* lists, int list_cap,
+                                      int32_t* list_count, void* stream) {
+  MISA_REQUIRE(lists && list_count, "null pointer");
+  MISA_REQUIRE(list_cap >= 1, "bad list capacity");
+  MISA_REQUIRE((reinterpret_cast<uintptr_t>(lists) & 15) == 0, "lists must be 16-byte aligned");
+  return refine_launch(keys, n_keys, head_dim, queries, weights, n_heads, n_heads_pad, cand, cand_ld, n_cand, rows,
+                       n_items, n_rows, row_key0, nullptr, lists, list_count, 4 * (int64_t)list_cap, stream);
 }
 
 extern "C" int misa_relevance_dots(const void* keys, int64_t n_keys, int head_dim, const void* queries, int n_queries,

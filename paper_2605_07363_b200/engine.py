@@ -622,19 +622,34 @@ class IndexerEngine:
         (rows,) = self._dev_list(("refine_rows", ckey, kp),  # schedule only: longest rows first
                                  lambda: (np.argsort(-np.minimum(x.prefix_host, kp), kind="stable").astype(np.int32),),
                                  dev)
-        rs = self._buf("refine_scores", (x.T, kp), torch.float32, dev)
         stream = self._stream()
-        self._mark("refine")
-        _lib.call("misa_refine_scores", _ptr(x.keys), x.n_keys, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
-                  _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(rows), rows.numel(), x.T,
-                  None if x.seq is None else _ptr(x.seq.key0), _ptr(rs), kp, stream)
-        self._mark("refine_select")
-        if runs is not None:
-            _lib.call("misa_select_dense_runs", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(runs),
-                      x.T, k, _ptr(out), out.stride(0), stream)
+        lc = kp // 4
+        if kp % 4 == 0 and lc in V5_CAPS and x.L <= 32 * 8192:  # topk5's chunk scan covers <= 8192 chunks
+            # scores packed as the fused selector's 4 candidate lists: the re-rank's top-k is then
+            # misa_select_topk (chunk-scan ordering), not a per-row CTA over a dense score row
+            lists = self._buf("refine_lists", (x.T, 4, lc), torch.int64, dev)
+            lcnt = self._buf("refine_lcnt", (x.T, 4), torch.int32, dev)
+            flags = self._buf("refine_flags", (x.T,), torch.int32, dev)
+            self._mark("refine")
+            _lib.call("misa_refine_candidates", _ptr(x.keys), x.n_keys, x.D, _ptr(x.queries), _ptr(x.weights), x.H,
+                      x.Hp, _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(rows), rows.numel(), x.T,
+                      None if x.seq is None else _ptr(x.seq.key0), _ptr(lists), lc, _ptr(lcnt), stream)
+            self._mark("refine_select")
+            _lib.call("misa_select_topk", _ptr(lists), _ptr(lcnt), lc, _ptr(x.prefix), x.T, k, x.L, _ptr(out),
+                      out.stride(0), None, _ptr(flags), stream)
         else:
-            _lib.call("misa_select_dense", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), None, x.T, k,
-                      _ptr(out), out.stride(0), None, stream)
+            rs = self._buf("refine_scores", (x.T, kp), torch.float32, dev)
+            self._mark("refine")
+            _lib.call("misa_refine_scores", _ptr(x.keys), x.n_keys, x.D, _ptr(x.queries), _ptr(x.weights), x.H,
+                      x.Hp, _ptr(cand), cand.stride(0), _ptr(ncand), _ptr(rows), rows.numel(), x.T,
+                      None if x.seq is None else _ptr(x.seq.key0), _ptr(rs), kp, stream)
+            self._mark("refine_select")
+            if runs is not None:
+                _lib.call("misa_select_dense_runs", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand),
+                          _ptr(runs), x.T, k, _ptr(out), out.stride(0), stream)
+            else:
+                _lib.call("misa_select_dense", _ptr(rs), kp, _ptr(cand), cand.stride(0), _ptr(ncand), None, x.T, k,
+                          _ptr(out), out.stride(0), None, stream)
         self._mark("refine:end")
 
     # ----------------------------------------------------------- decode
