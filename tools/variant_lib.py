@@ -20,18 +20,20 @@ if sys.argv[1] == "--run":
     Q = torch.randn(L, 64, 128, device="cuda", generator=g).bfloat16()
     W = torch.softmax(torch.randn(L, 64, device="cuda", generator=g), -1).float()
     x = prepare_inputs(K, Q, W)
-    eng = IndexerEngine("misa_hier")
-    for _ in range(2):
-        eng.run_prepared(x)
-    st = {}
-    for _ in range(3):
-        eng.stage_events = []
-        eng.run_prepared(x)
-        torch.cuda.synchronize()
-        ev = eng.stage_events
-        for (n0, e0), (_, e1) in zip(ev, ev[1:]):
-            st[n0] = st.get(n0, 0.0) + e0.elapsed_time(e1) / 3
-    print(sys.argv[2], {k: round(v, 3) for k, v in st.items()})
+    for method in ("misa", "dsa", "misa_hier"):
+        eng = IndexerEngine(method)
+        for _ in range(2):
+            eng.run_prepared(x)
+        st = {}
+        for _ in range(3):
+            eng.stage_events = []
+            eng.run_prepared(x)
+            torch.cuda.synchronize()
+            ev = eng.stage_events
+            for (n0, e0), (_, e1) in zip(ev, ev[1:]):
+                st[n0] = st.get(n0, 0.0) + e0.elapsed_time(e1) / 3
+        print(sys.argv[2], method, {k: round(v, 3) for k, v in st.items()}, flush=True)
+        del eng
 else:
     from paper_2605_07363_b200 import _build
     out, flags = sys.argv[1], sys.argv[2:]
