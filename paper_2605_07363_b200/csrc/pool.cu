@@ -1,7 +1,7 @@
 // K1: block pooling of indexer keys (pooling.py:57-84) and its decode update
 // (pooling.py:87-115).
 //
-// One CTA per B-key block.  Each thread owns 8 head dims (one 16-byte bf16
+// CTAs per (B-key block, 32 head dims).  Each thread owns 8 head dims (one 16-byte bf16
 // vector) of a strided sub-segment of the block, so every warp load is a
 // coalesced 512-byte row span.  Three phases: sub-segment sums -> exclusive
 // carry across sub-segments (smem) -> re-walk writing the in-block inclusive
@@ -26,14 +26,18 @@ __device__ __forceinline__ void split3_store(__nv_bfloat16* planes, int64_t plan
   planes[(2 * planes_rows + b) * D + dim] = lo;
 }
 
+// grid (blocks, D / 32): a CTA pools 32 head dims (4 x 16-byte vectors per key row) of one
+// block over 64 sub-segments, so a layer launches blocks x D/32 CTAs (every SM busy even at
+// 32 blocks) and each thread walks only ceil(B / 64) keys.
 template <int D>
 __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restrict__ keys, int64_t L, int B,
                                                     float* __restrict__ prefix, float* __restrict__ pooled,
                                                     __nv_bfloat16* __restrict__ planes, int64_t planes_rows) {
-  constexpr int CH = D / 8;        // threads per key row
+  constexpr int CH = 4;            // threads per key row (32 dims of this CTA)
   constexpr int RP = 256 / CH;     // sub-segments
-  __shared__ float sums[RP][D];
+  __shared__ float sums[RP][32 + 1];
   const int b = blockIdx.x;
+  const int d0 = blockIdx.y * 32;
   const int64_t start = (int64_t)b * B;
   const int len = (int)((start + B <= L) ? B : (L - start));
   const int sr = threadIdx.x / CH, ch = threadIdx.x % CH;
@@ -43,12 +47,14 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
   // key buffer)
   const int seg = (B + RP - 1) / RP;
   const int s0 = sr * seg, s1 = min(len, s0 + seg);
+  const __nv_bfloat16* kb = keys + start * D + d0 + ch * 8;
 
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll 4
   for (int s = s0; s < s1; ++s) {
-    const uint4 v = *reinterpret_cast<const uint4*>(keys + (start + s) * D + ch * 8);
+    const uint4 v = *reinterpret_cast<const uint4*>(kb + (int64_t)s * D);
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -68,8 +74,9 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
     for (int r = 0; r < sr; ++r)
 #pragma unroll
       for (int i = 0; i < 8; ++i) run[i] += sums[r][ch * 8 + i];
+#pragma unroll 4
     for (int s = s0; s < s1; ++s) {
-      const uint4 v = *reinterpret_cast<const uint4*>(keys + (start + s) * D + ch * 8);
+      const uint4 v = *reinterpret_cast<const uint4*>(kb + (int64_t)s * D);
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -77,7 +84,7 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
         run[2 * i] += f.x;
         run[2 * i + 1] += f.y;
       }
-      float4* dst = reinterpret_cast<float4*>(prefix + (start + s) * D + ch * 8);
+      float4* dst = reinterpret_cast<float4*>(prefix + (start + s) * D + d0 + ch * 8);
       dst[0] = make_float4(run[0], run[1], run[2], run[3]);
       dst[1] = make_float4(run[4], run[5], run[6], run[7]);
     }
@@ -90,7 +97,7 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
       float tot = 0.f;
       for (int r = 0; r < RP; ++r) tot += sums[r][ch * 8 + i];
       const float m = tot * inv;
-      const int dim = ch * 8 + i;
+      const int dim = d0 + ch * 8 + i;
       if (pooled) pooled[(int64_t)b * D + dim] = m;
       if (planes) split3_store(planes, planes_rows, b, D, dim, m);
     }
@@ -138,9 +145,9 @@ extern "C" int misa_pool_keys(const void* keys, int64_t n_keys, int head_dim, in
   auto* k = static_cast<const __nv_bfloat16*>(keys);
   auto* pl = static_cast<__nv_bfloat16*>(pooled_planes);
   if (head_dim == 128)
-    pool_kernel<128><<<(unsigned)nb, 256, 0, st>>>(k, n_keys, block_size, prefix_sums, pooled, pl, planes_rows);
+    pool_kernel<128><<<dim3((unsigned)nb, 128 / 32), 256, 0, st>>>(k, n_keys, block_size, prefix_sums, pooled, pl, planes_rows);
   else
-    pool_kernel<64><<<(unsigned)nb, 256, 0, st>>>(k, n_keys, block_size, prefix_sums, pooled, pl, planes_rows);
+    pool_kernel<64><<<dim3((unsigned)nb, 64 / 32), 256, 0, st>>>(k, n_keys, block_size, prefix_sums, pooled, pl, planes_rows);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }

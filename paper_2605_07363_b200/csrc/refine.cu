@@ -301,6 +301,13 @@ __global__ void __launch_bounds__(kRefThreads, 1)
         for (int j = first; j < nt; j += kRefSets) {
           const int gg = g + j;
           const int acc = gg % kRefAcc;
+          // packed output: this lane's candidate key, loaded before the wait so its L2 latency
+          // overlaps the MMA instead of the epilogue chain
+          uint32_t pkey = 0;
+          if (!DOTS && a.out64) {
+            const int i = j * 128 + quad * 32 + lane;
+            if (i < nc) pkey = static_cast<uint32_t>(__ldg(a.cand + (int64_t)t * a.cand_ld + i));
+          }
           ptx::mbar_wait(&tfull[acc], (gg / kRefAcc) & 1);
           __syncwarp();  // reconverge before the warp-collective TMEM loads
           ptx::tc_fence_after();
@@ -359,11 +366,9 @@ __global__ void __launch_bounds__(kRefThreads, 1)
           const float sc = gate_relu_finish(s0, s1);
           const int i = j * 128 + quad * 32 + lane;
           if (a.out64) {
-            if (i < nc) {
-              const uint32_t key = static_cast<uint32_t>(__ldg(a.cand + (int64_t)t * a.cand_ld + i));
+            if (i < nc)
               __stcs(reinterpret_cast<unsigned long long*>(a.out64 + (int64_t)t * a.out_ld + i),
-                     (static_cast<unsigned long long>(key) << 32) | __float_as_uint(sc));
-            }
+                     (static_cast<unsigned long long>(pkey) << 32) | __float_as_uint(sc));
             if (j == 0 && quad == 0 && lane < 4) {
               const int c = nc - lane * a.list_cap;
               a.list_count[(int64_t)t * 4 + lane] = c < 0 ? 0 : (c > a.list_cap ? a.list_cap : c);

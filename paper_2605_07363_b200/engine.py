@@ -548,6 +548,7 @@ class IndexerEngine:
                   append_all, _ptr(tau), stream)
         cand = self._buf(tag + "_cand", (x.T * 4 * cap,), torch.int64, dev)
         cnt = self._buf(tag + "_cnt", (x.T * 4,), torch.int32, dev)
+        cnt.zero_()  # rows without a filter item (n <= k) keep defined counts (the selector prefetches them)
         if f_items.numel():
             self._mark(tag + ":filter")
             if x.seq is None:
@@ -571,9 +572,11 @@ class IndexerEngine:
         self._mark(tag + ":end")
         if not self.check_overflow:
             return 0
-        bad = torch.nonzero(flags).flatten()
-        if bad.numel() == 0:
+        # one reduction + one 4-byte read on the common (no flagged row) path; the row list
+        # (a device-wide select + size sync) only when some row was flagged
+        if int(flags.amax().item()) == 0:
             return 0
+        bad = torch.nonzero(flags).flatten()
         self._dense_rows(x, heads, hq, k, out, bad.cpu().numpy(), scores)
         if runs is not None:  # re-selected rows are ascending: one run
             runs[bad] = 0
