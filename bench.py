@@ -352,7 +352,7 @@ def run_ours(a):
             Ps = Ls * (Ls + 1) // 2
             sweep.append({"workload": name, "misa_ms": round(ms_m, 3), "dsa_ms": round(ms_d, 3),
                           "speedup_vs_dsa": round(ms_d / ms_m, 3), "misa_scores_per_s": Ps / (ms_m * 1e-3),
-                          "misa_tensor_frac": round(2.0 * a.h * a.d * Ps / (ms_m * 1e-3) / 1e12 / tc_sust, 4)})
+                          "misa_tensor_frac_burst": round(2.0 * a.h * a.d * Ps / (ms_m * 1e-3) / 1e12 / tc_burst, 4)})
             del Ks, Qs, Ws, xs, em, ed
 
     hier_ms = None
