@@ -25,6 +25,7 @@
  *   misa_score_materialize_split  the same, key-axis split (decode)
  *   misa_score_materialize_paged  the same over a paged key cache (decode)
  *   misa_score_filter     dsa.py:37-76 fused with the candidate pass of topk_tokens
+ *   misa_score_filter_split  the same over key-split items (decode)
  *   misa_select_threshold (no reference counterpart: sampled threshold for the fused top-k)
  *   misa_select_topk      dsa.py:64-76       topk_tokens over the filtered candidates
  *   misa_select_topk_runs routing.py:157-159 the coarse top-k' set of misa_hier_select (unordered runs)
@@ -206,6 +207,10 @@ int misa_select_topk_runs(const uint64_t* cand, const int32_t* cand_count, int c
                           int64_t n_rows, int k, int64_t max_prefix_len, int32_t* topk, int64_t topk_ld,
                           int32_t* runs, int32_t* flags, void* stream);
 
+/* Ascending sort, in place, of each row's first min(k, prefix_len[t]) entries (k <= 16384):
+ * the ordering step after an unordered selection. */
+int misa_sort_rows(int32_t* rows, int64_t ld, const int32_t* prefix_len, int64_t n_rows, int k, void* stream);
+
 /* misa_select_dense over rows made of 4 ascending runs (runs[t*4 + q] lengths, summing to
  * row_len[t]) with explicit indices idx: the top-k (score desc, index asc), ascending. */
 int misa_select_dense_runs(const float* scores, int64_t ld, const int32_t* idx, int64_t idx_ld,
@@ -247,6 +252,17 @@ int misa_refine_candidates(const void* keys, int64_t n_keys, int head_dim, const
                            const int32_t* n_cand, const int32_t* rows, int n_items, int64_t n_rows,
                            const int32_t* row_key0, uint64_t* lists, int list_cap, int32_t* list_count,
                            void* stream);
+
+/* misa_score_filter over key-split work items (decode: a few rows against long prefixes, every
+ * SM busy): item i scores rows group items[i] over key tiles [item_tile0[i], +item_tiles[i]).
+ * cand_count must be zeroed: each warp reserves its 32-key chunk's slots of a (row, quadrant)
+ * list with one atomicAdd, so chunks are contiguous and ascending inside a list (chunk order
+ * within a list is arbitrary; misa_select_topk's ordering needs no more). */
+int misa_score_filter_split(const void* keys, int64_t n_keys, int head_dim, const void* queries, const float* weights,
+                            int n_heads, int n_heads_pad, const int32_t* heads, int heads_per_query,
+                            const int32_t* prefix_len, int64_t n_rows, const int32_t* items,
+                            const int32_t* item_tiles, const int32_t* item_tile0, int n_items, const float* tau,
+                            uint64_t* cand, int cap, int32_t* cand_count, void* stream);
 
 /* Multi-GPU merge: n_parts local (score, index) top-k lists per row (parts[p][t][i], scores
  * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc).

@@ -148,6 +148,11 @@ struct ScoreArgs {
   uint64_t* cand;
   int cap;
   int32_t* cand_count;
+  // FILTER over key-split items (several items per row, misa_score_filter_split): each warp
+  // reserves its tile's slots of a (row, quadrant) list with one atomicAdd on the zeroed
+  // cand_count, so a 32-key chunk's candidates stay contiguous and ascending (the selector's
+  // chunk-scan order needs no more) while the chunks of a list come in any order
+  int cand_atomic;
 };
 
 template <int D, int HQ>
@@ -392,6 +397,20 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
               pair_ballots<true>(sc, kq + rr, tau_a, tau_b, sLim + qa, bal);
             else
               pair_ballots<false>(sc, kq + rr, tau_a, tau_b, sLim + qa, bal);
+            if (a.cand_atomic) {
+              // this tile's slots of rows qa / qa+1 (quadrant quad): lane m reserves for its pair group
+#pragma unroll
+              for (int b = 0; b < 2; ++b) {
+                int tot = 0;
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4) tot += __popc(bal[s4][b] & gm);
+                int base = 0;
+                if (lane == m && tot > 0)
+                  base = atomicAdd(a.cand_count + (static_cast<int64_t>(row0 + qa + b) * kQuadrants + quad), tot);
+                base = __shfl_sync(0xffffffffu, base, m);
+                (b ? cnt_b : cnt_a) = base;
+              }
+            }
 #pragma unroll
             for (int s4 = 0; s4 < 4; ++s4) {
               const uint32_t key = static_cast<uint32_t>(kq + rr + 8 * s4);
@@ -419,7 +438,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
           }
         }
         if constexpr (FILTER) {
-          if (rr == 0) {
+          if (rr == 0 && !a.cand_atomic) {
 #pragma unroll
             for (int b = 0; b < 2; ++b) {
               const int row = row0 + qa + b;
@@ -478,6 +497,16 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
               pass_ballots<QW, true>(sc, key, sTau + qbase, sLim + qbase, bal);
             else
               pass_ballots<QW, false>(sc, key, sTau + qbase, sLim + qbase, bal);
+            if (a.cand_atomic) {
+#pragma unroll
+              for (int q = 0; q < QW; ++q) {
+                const int tot = __popc(bal[q]);
+                int base = 0;
+                if (lane == 0 && tot > 0)
+                  base = atomicAdd(a.cand_count + (static_cast<int64_t>(row0 + qbase + q) * kQuadrants + quad), tot);
+                cnt[q] = __shfl_sync(0xffffffffu, base, 0);
+              }
+            }
   #pragma unroll
             for (int q = 0; q < QW; ++q) {
               const int pos = cnt[q] + __popc(bal[q] & lt);
@@ -497,7 +526,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
   #pragma unroll
           for (int q = 0; q < QW; ++q)
             if (lane == q) mine = cnt[q];
-          if (lane < QW) {
+          if (lane < QW && !a.cand_atomic) {
             const int row = row0 + qbase + lane;
             if (row < row_end) a.cand_count[(int64_t)row * kQuadrants + quad] = mine;
           }
@@ -676,6 +705,41 @@ extern "C" int misa_score_filter(const void* keys, int64_t n_keys, int head_dim,
   a.cand = cand;
   a.cap = cap;
   a.cand_count = cand_count;
+  return dispatch_score<true>(head_dim, heads_per_query, map, a, as_stream(stream));
+}
+
+extern "C" int misa_score_filter_split(const void* keys, int64_t n_keys, int head_dim, const void* queries,
+                                       const float* weights, int n_heads, int n_heads_pad, const int32_t* heads,
+                                       int heads_per_query, const int32_t* prefix_len, int64_t n_rows,
+                                       const int32_t* items, const int32_t* item_tiles, const int32_t* item_tile0,
+                                       int n_items, const float* tau, uint64_t* cand, int cap, int32_t* cand_count,
+                                       void* stream) {
+  int rc = check_common(n_keys, head_dim, n_heads, n_heads_pad, heads_per_query, n_rows, keys, queries, weights,
+                        prefix_len, items, item_tiles, n_items);
+  if (rc) return rc;
+  MISA_REQUIRE(tau && cand && cand_count && cap >= 1 && (item_tile0 || n_items == 0), "null filter buffers");
+  MISA_REQUIRE(heads != nullptr || heads_per_query >= n_heads, "dense scoring needs heads_per_query >= n_heads");
+  CUtensorMap map;
+  rc = make_tmap_bf16_2d(&map, keys, head_dim, n_keys, head_dim, kTileKeys);
+  if (rc) return rc;
+  ScoreArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(queries);
+  a.w = weights;
+  a.heads = heads;
+  a.prefix_len = prefix_len;
+  a.items = items;
+  a.item_tiles = item_tiles;
+  a.item_tile0 = item_tile0;
+  a.n_items = n_items;
+  a.T = static_cast<int>(n_rows);
+  a.H = n_heads;
+  a.Hp = n_heads_pad;
+  a.key_stride = 1;
+  a.tau = tau;
+  a.cand = cand;
+  a.cap = cap;
+  a.cand_count = cand_count;
+  a.cand_atomic = 1;
   return dispatch_score<true>(head_dim, heads_per_query, map, a, as_stream(stream));
 }
 

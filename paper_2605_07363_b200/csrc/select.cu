@@ -2091,7 +2091,7 @@ static int launch_topk5(cudaStream_t st, const uint64_t* cand, const int32_t* cc
                         int64_t T, int k, int64_t max_n, int32_t* topk, int64_t ld, float* ts, int32_t* flags,
                         int32_t* runs = nullptr) {
   const int64_t n_chunks = (max_n + 31) / 32;
-  if (n_chunks > 8192 || cap > 0xffff) return -100;
+  if ((!runs && n_chunks > 8192) || cap > 0xffff) return -100;  // unordered: no chunk histogram
   const int nc = static_cast<int>(n_chunks);
   // NT*EPT == 4*cap with cap a multiple of 32*EPT*(NT/128)
 #define MISA_TOPK5_CASE(NT_, EPT_) \
@@ -2105,6 +2105,37 @@ static int launch_topk5(cudaStream_t st, const uint64_t* cand, const int32_t* cc
   MISA_TOPK5_CASE(512, 32)
 #undef MISA_TOPK5_CASE
   return -100;
+}
+
+// Ascending sort of each row's first min(k, n_t) entries (bitonic in shared memory, P = the
+// next power of two, padded with INT_MAX): turns an unordered selection (misa_select_topk_runs
+// over lists whose chunks arrive in any order, e.g. key-split decode) into topk_tokens' output.
+template <int NT>
+__global__ void __launch_bounds__(NT) sort_rows_kernel(int32_t* __restrict__ rows, int64_t ld,
+                                                      const int32_t* __restrict__ prefix_len, int k, int P) {
+  extern __shared__ int32_t sv[];
+  const int t = blockIdx.x;
+  const int n = prefix_len[t];
+  const int kk = n < k ? (n > 0 ? n : 0) : k;
+  int32_t* row = rows + (int64_t)t * ld;
+  for (int i = threadIdx.x; i < P; i += NT) sv[i] = i < kk ? row[i] : 0x7fffffff;
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P / 2; i += NT) {
+        const int lo = 2 * i - (i & (stride - 1));  // index with bit `stride` clear
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const int32_t a = sv[lo], b = sv[hi];
+        if ((a > b) == up) {
+          sv[lo] = b;
+          sv[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < kk; i += NT) row[i] = sv[i];
 }
 
 // runs[t] = (min(k, n_t), 0, 0, 0): one ascending run (rows selected by an ordered path)
@@ -2123,6 +2154,19 @@ extern "C" int misa_select_threshold(const float* sample_scores, int64_t ld, con
                                      float* tau, void* stream) {
   MISA_REQUIRE(sample_scores && prefix_len && tau, "null pointer");
   MISA_REQUIRE(k >= 1 && key_stride >= 1 && beta > 0.f && n_rows >= 1, "bad threshold arguments");
+  // few rows (decode): one CTA per row over the contiguous sample (a warp per row would be
+  // latency-bound: ~36 us for one 16384-sample row)
+  if (n_rows * 2 <= sm_count() && ld <= 1024 * 16) {
+    cudaStream_t st = as_stream(stream);
+    if (ld <= 512 * 16)
+      threshold_kernel<512, 16><<<(unsigned)n_rows, 512, 0, st>>>(sample_scores, ld, prefix_len, (int)n_rows,
+                                                                  key_stride, k, beta, append_all_len, tau, 1);
+    else
+      threshold_kernel<1024, 16><<<(unsigned)n_rows, 1024, 0, st>>>(sample_scores, ld, prefix_len, (int)n_rows,
+                                                                    key_stride, k, beta, append_all_len, tau, 1);
+    MISA_LAUNCH_CHECK();
+    return MISA_OK;
+  }
   // one warp per row: 32 KB of histograms per 4-warp CTA, 6 CTAs (24 rows) per SM
   constexpr int WARPS = 4;
   auto kern = threshold_warp_kernel<WARPS>;
@@ -2167,6 +2211,20 @@ extern "C" int misa_select_topk_runs(const uint64_t* cand, const int32_t* cand_c
                                   nullptr, flags, stream);
   if (rc) return rc;
   single_run_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, as_stream(stream)>>>(prefix_len, n_rows, k, runs);
+  MISA_LAUNCH_CHECK();
+  return MISA_OK;
+}
+
+extern "C" int misa_sort_rows(int32_t* rows, int64_t ld, const int32_t* prefix_len, int64_t n_rows, int k,
+                              void* stream) {
+  MISA_REQUIRE(rows && prefix_len, "null pointer");
+  MISA_REQUIRE(k >= 1 && k <= 16384 && ld >= k && n_rows >= 0, "bad sort arguments (k <= 16384)");
+  if (n_rows == 0) return MISA_OK;
+  int P = 1;
+  while (P < k) P <<= 1;
+  const size_t bytes = (size_t)P * 4;
+  MISA_CUDA_TRY(cudaFuncSetAttribute(sort_rows_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  sort_rows_kernel<1024><<<(unsigned)n_rows, 1024, bytes, as_stream(stream)>>>(rows, ld, prefix_len, k, P);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }

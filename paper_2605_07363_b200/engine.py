@@ -329,6 +329,14 @@ class IndexerEngine:
         self._ws: dict = {}
         self._lists: dict = {}
         self.last_fallback_rows = 0
+        # decode steps with at least this many rows and keys score through the fused filter (no
+        # T x L score rows in HBM); others take the materialised key-split path.  Measured on a
+        # B200 (graph replay, no flag check): 1M keys x 64 rows 0.26 vs 0.31 ms, but 128K x 64
+        # 0.135 vs 0.092 and 1M x 16 0.17 vs 0.14 — the sample / tau / select / sort chain costs
+        # more than the score rows it saves below that size
+        self.decode_filter_min_rows = 32
+        self.decode_filter_min_keys = 1 << 19
+        self.last_decode_flags = None  # (T,) flags of the last fused-filter decode step (None: dense path)
         self.stage_events: list | None = None  # set to [] to record (stage, cuda event) pairs
         _lib.load()
 
@@ -721,6 +729,58 @@ class IndexerEngine:
                   float(beta), _ptr(tau), _ptr(seg), _ptr(cs), _ptr(ci), _ptr(cc), cap, _ptr(out), out.stride(0),
                   _ptr(scores), self._stream())
 
+    def decode_filter_select(self, x: PreparedInputs, heads, hq: int, k: int, out: torch.Tensor):
+        """Decode rows through the fused filter: a 1/stride key sample scored on every SM gives
+        tau_t (a CTA per row), the key-split filter scorer appends (score, key) >= tau_t to the
+        row's four candidate lists (slots reserved per 32-key chunk with one atomic), the
+        selector cuts the exact top-k (unordered runs) and a row sort restores topk_tokens'
+        ascending order.  No T x L score rows touch HBM.  Returns the (T,) flags of rows whose
+        candidates under/overflowed (to be re-selected exactly), or None when the shape falls
+        outside the compiled selector (caller takes the dense path)."""
+        dev = x.keys.device
+        if x.pages is not None or x.seq is not None:
+            return None
+        stride = max(32, -(-x.L // 16384))
+        beta = 2.0 if k < 4096 else 1.2
+        j = max(1.0, beta * k / stride)
+        cap = int(math.ceil((1.0 + 5.5 / math.sqrt(j)) * beta * k / 4 / 32)) * 32
+        cap = next((c for c in V5_CAPS if c >= cap), None)
+        if cap is None:
+            return None
+        G = 256 // hq
+        target = 4 * _lib.load().misa_sm_count()
+        ckey = x.list_key()
+        m = -(-x.L // stride)
+        lens_s = -(-x.prefix_host // stride)
+        s_items, s_tiles, s_tile0 = self._dev_list(("dsamp", ckey, G, target, stride),
+                                                   lambda: self.split_items(lens_s, G, target), dev)
+        samp = self._buf("dec_samp", (x.T, m), torch.float32, dev)
+        stream = self._stream()
+        self._mark("decode:sample")
+        _lib.call("misa_score_materialize_split", _ptr(x.keys), x.L, stride, x.D, _ptr(x.queries), _ptr(x.weights),
+                  x.H, x.Hp, _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(s_items), _ptr(s_tiles), _ptr(s_tile0),
+                  s_items.numel(), _ptr(samp), m, stream)
+        tau = self._buf("dec_tau", (x.T,), torch.float32, dev)
+        self._mark("decode:threshold")
+        _lib.call("misa_select_threshold", _ptr(samp), m, _ptr(x.prefix), x.T, stride, k, float(beta), 4 * cap,
+                  _ptr(tau), stream)
+        cand = self._buf("dec_cand", (x.T * 4 * cap,), torch.int64, dev)
+        cnt = self._buf("dec_cnt", (x.T * 4,), torch.int32, dev)
+        cnt.zero_()
+        items, tiles, tile0 = self._dev_list(("split", ckey, G, target),
+                                             lambda: self.split_items(x.prefix_host, G, target), dev)
+        self._mark("decode:filter")
+        _lib.call("misa_score_filter_split", _ptr(x.keys), x.L, x.D, _ptr(x.queries), _ptr(x.weights), x.H, x.Hp,
+                  _ptr(heads), hq, _ptr(x.prefix), x.T, _ptr(items), _ptr(tiles), _ptr(tile0), items.numel(),
+                  _ptr(tau), _ptr(cand), cap, _ptr(cnt), stream)
+        flags = self._buf("dec_flags", (x.T,), torch.int32, dev)
+        runs = self._buf("dec_runs", (x.T, 4), torch.int32, dev)
+        self._mark("decode:select")
+        _lib.call("misa_select_topk_runs", _ptr(cand), _ptr(cnt), cap, _ptr(x.prefix), x.T, k, x.L, _ptr(out),
+                  out.stride(0), _ptr(runs), _ptr(flags), stream)
+        _lib.call("misa_sort_rows", _ptr(out), out.stride(0), _ptr(x.prefix), x.T, k, stream)
+        return flags
+
     def decode(self, keys=None, queries=None, weights=None, prefix_len=None, *, cache=None,
                need_importance: bool = False, out: torch.Tensor | None = None) -> IndexerOutput:
         """Decode step: a few query rows (T <= a few hundred) against long prefixes.
@@ -760,9 +820,18 @@ class IndexerEngine:
             heads, hq, imp = self.route(x, need_importance, cache=cache)
         kk = k if self.method != "misa_hier" else max(self.kprime, k)
         tgt = out if self.method != "misa_hier" else self._buf("hier_cand", (x.T, kk), torch.int32, dev)
-        self.dense_select(x, heads, hq, kk, tgt)
-        self._mark("decode:end")
+        flags = None
+        if x.T >= self.decode_filter_min_rows and x.L >= self.decode_filter_min_keys:
+            flags = self.decode_filter_select(x, heads, hq, kk, tgt)
+        if flags is None:
+            self.dense_select(x, heads, hq, kk, tgt)
+        self.last_decode_flags = flags
         self.last_fallback_rows = 0
+        if flags is not None and not torch.cuda.is_current_stream_capturing():
+            # eager: flagged rows (candidate under/overflow) are re-selected exactly on the
+            # dense path; under a CUDA graph DecodeGraph.step checks the flags after replay
+            self.last_fallback_rows = self.fix_decode_rows(x, heads, hq, kk, tgt, flags)
+        self._mark("decode:end")
         h = min(self.h, x.H)
         if self.method == "dsa":
             return IndexerOutput(topk=out)
@@ -771,6 +840,14 @@ class IndexerEngine:
         self.refine(x, tgt, k, out)
         return IndexerOutput(topk=out, heads=heads[:, :h], importance=None if imp is None else imp[:, :x.H],
                              candidates=tgt)
+
+    def fix_decode_rows(self, x: PreparedInputs, heads, hq: int, k: int, out: torch.Tensor, flags) -> int:
+        """Exact re-selection of the rows a fused-filter decode step flagged (host check)."""
+        if int(flags.amax().item()) == 0:
+            return 0
+        bad = torch.nonzero(flags).flatten().cpu().numpy()
+        self._dense_rows(x, heads, hq, k, out, bad)
+        return int(bad.shape[0])
 
     # ----------------------------------------------------------- host pipeline
     def run_host(self, keys, queries, weights, prefix_len=None, *, chunks: int = 8,
@@ -992,6 +1069,9 @@ class DecodeGraph:
         self.graph = None
         self.Lb = 0
         self.result = None
+        self._x = None
+        self._flag_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)  # fused-filter steps: max flag
+        self._checks = False
 
     def _capture(self, Lb: int) -> None:
         c = self.cache
@@ -1013,6 +1093,11 @@ class DecodeGraph:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
             self.result = eng.decode_prepared(x, cache=c, out=self.out)
+            fl = eng.last_decode_flags
+            self._checks = fl is not None
+            if self._checks:  # the step's flag summary lands in pinned memory inside the graph
+                self._flag_host.copy_(fl.amax().view(1), non_blocking=True)
+        self._x = x
         # the graph holds raw device pointers into the engine's workspace and cached work
         # lists: keep those tensors alive for the graph's lifetime, even if a later eager call
         # on the same engine swaps in larger buffers or clears the work-list cache
@@ -1031,4 +1116,15 @@ class DecodeGraph:
         self.w[:, :self.H].copy_(weights, non_blocking=True)
         self.prefix.fill_(L)
         self.graph.replay()
+        if self._checks:
+            # a fused-filter step is exact unless a row's candidates under/overflowed: then the
+            # whole step is re-run eagerly on the dense path (rare; keeps every step exact)
+            torch.cuda.current_stream().synchronize()
+            if int(self._flag_host.item()):
+                eng = self.engine
+                keep, eng.decode_filter_min_rows = eng.decode_filter_min_rows, 1 << 30
+                try:
+                    self.result = eng.decode_prepared(self._x, cache=self.cache, out=self.out)
+                finally:
+                    eng.decode_filter_min_rows = keep
         return self.result

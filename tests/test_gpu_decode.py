@@ -264,3 +264,54 @@ def test_decode_graph_over_paged_cache():
                                                                                        cache=cache)
         torch.cuda.synchronize()
         assert torch.equal(got.topk, ref.topk) and torch.equal(got.heads, ref.heads), L
+
+
+@pytest.mark.parametrize("method,L,T", [("misa", 300000, 16), ("dsa", 70000, 8), ("misa_hier", 50000, 12),
+                                        ("misa", 5000, 9)])
+def test_decode_fused_filter_equals_dense_path(method, L, T):
+    """Decode rows through the fused filter (sample -> tau -> key-split filter with atomic slot
+    reservation -> unordered cut -> row sort) == the materialised dense path, bit for bit;
+    L > 262144 exercises the unordered selector past topk5's chunk-scan range."""
+    from paper_2605_07363_b200 import IndexerEngine
+    K, Q, W = _inputs(L, T, seed=11)
+    rng = np.random.default_rng(1)
+    pl = rng.integers(max(1, L // 3), L + 1, T)
+    pl[0], pl[-1] = L, min(L, 700)
+    kw = dict(budget_k=512, active_heads_h=8, block_size=1024, candidate_kprime=2048)
+    fused = IndexerEngine(method, **kw)
+    fused.decode_filter_min_rows, fused.decode_filter_min_keys = 1, 1
+    dense = IndexerEngine(method, **kw)
+    dense.decode_filter_min_rows = 1 << 30
+    a = fused.decode(K, Q, W, prefix_len=pl)
+    assert fused.last_decode_flags is not None
+    b = dense.decode(K, Q, W, prefix_len=pl)
+    torch.cuda.synchronize()
+    assert torch.equal(a.topk, b.topk)
+    if method == "misa_hier":
+        assert torch.equal(a.candidates, b.candidates)
+
+
+def test_decode_fused_filter_flagged_rows_are_exact():
+    """All-equal keys: every score ties, every key passes tau, the candidate lists overflow and
+    the rows are flagged; eager decode and DecodeGraph re-select them exactly (ties -> smaller
+    index: the first k keys)."""
+    from paper_2605_07363_b200 import DecodeGraph, IndexerEngine
+    from paper_2605_07363_b200.pooling import PooledKeyCache
+    L, T, k = 40000, 8, 256
+    _, Q, W = _inputs(L, T, seed=13)
+    K = torch.ones(L, 128, device="cuda").bfloat16()
+    eng = IndexerEngine("misa", budget_k=k, active_heads_h=8, block_size=1024)
+    eng.decode_filter_min_rows, eng.decode_filter_min_keys = 1, 1
+    out = eng.decode(K, Q, W)
+    torch.cuda.synchronize()
+    assert eng.last_fallback_rows > 0
+    exp = torch.arange(k, dtype=torch.int32, device="cuda").expand(T, k)
+    assert torch.equal(out.topk, exp)
+    cache = PooledKeyCache(128, 1024, capacity=L)
+    cache.append(K)
+    eg = IndexerEngine("misa", budget_k=k, active_heads_h=8, block_size=1024)
+    eg.decode_filter_min_rows, eg.decode_filter_min_keys = 1, 1
+    dg = DecodeGraph(eg, cache, T, 64)
+    r = dg.step(Q, W)
+    torch.cuda.synchronize()
+    assert torch.equal(r.topk, exp)
