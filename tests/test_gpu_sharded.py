@@ -9,11 +9,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def test_two_rank_sharded_prefill_and_decode_equal_single_gpu():
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_prefill_and_decode_equal_single_gpu(world):
+    """world = 4 adds MISA-dagger at k' = 8192 with merge rounds (4 x 8192 > 16384)."""
     import subprocess
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, os.path.join(repo, "tools", "sharded_smoke.py")], capture_output=True,
-                       text=True, timeout=900)
+    r = subprocess.run([sys.executable, os.path.join(repo, "tools", "sharded_smoke.py"), str(world)],
+                       capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0 and "sharded smoke ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 

@@ -20,7 +20,7 @@ def worker(rank, world, port, q):
     Q = torch.randn(L, H, d, device="cuda", generator=g).bfloat16()
     W = torch.softmax(torch.randn(L, H, device="cuda", generator=g), -1).float()
     ok = {}
-    for m in ("misa", "dsa", "misa_hier"):
+    for m in (("misa", "dsa", "misa_hier") if world == 2 else ("misa",)):
         kw = dict(budget_k=k, active_heads_h=8, block_size=B, candidate_kprime=2048)
         ref = IndexerEngine(m, **kw).run(K, Q, W).topk
         sh = ShardedIndexer(m, world=world, rank=rank, **kw)
@@ -43,17 +43,22 @@ def worker(rank, world, port, q):
     sh = ShardedIndexer("misa_hier", world=world, rank=rank, **kw)
     ok["misa_hier_k8192_prefill"] = bool(torch.equal(sh.run(K, Q, W, gather=True), ref))
     ok["pruned"] = sh.exchange.last.get("cols", 8192) < 8192
+    if world > 2:  # G * k' = 32768 > 16384: the global merge runs in rounds of list groups
+        ok["misa_hier_k8192_decode"] = bool(torch.equal(sh.decode(K, Q[-8:].contiguous(), W[-8:].contiguous()),
+                                                        IndexerEngine("misa_hier", **kw).decode(
+                                                            K, Q[-8:].contiguous(), W[-8:].contiguous()).topk))
     q.put((rank, ok))
     dist.destroy_process_group()
 
 
 if __name__ == "__main__":
     s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    world = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
     [p.start() for p in ps]
-    res = dict(q.get(timeout=600) for _ in range(2))
+    res = dict(q.get(timeout=900) for _ in range(world))
     [p.join() for p in ps]
     print(res)
     assert all(all(v.values()) for v in res.values()), res
