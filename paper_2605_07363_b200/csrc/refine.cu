@@ -50,8 +50,14 @@ struct RefineArgs {
 constexpr int kRefGroups = MISA_REF_GROUPS;              // independent producer groups
 constexpr int kRefGroupWarps = 2;                        // warps per group (64 tile rows each)
 constexpr int kRefProd = kRefGroups * kRefGroupWarps;    // cp.async producer warps
-constexpr int kRefAcc = 4;                               // TMEM accumulators (ring)
-constexpr int kRefSets = 2;                              // epilogue warp sets (set = tile % kRefSets)
+#ifndef MISA_REF_ACC
+#define MISA_REF_ACC 4
+#endif
+#ifndef MISA_REF_SETS
+#define MISA_REF_SETS 2
+#endif
+constexpr int kRefAcc = MISA_REF_ACC;                    // TMEM accumulators (ring)
+constexpr int kRefSets = MISA_REF_SETS;                  // epilogue warp sets (set = tile % kRefSets)
 constexpr int kRefMma = kRefProd;                        // MMA warp index
 constexpr int kRefBLoad = kRefProd + 1;                  // B (queries + gates) loader warp
 constexpr int kRefEpi0 = kRefProd + 2;                   // first epilogue warp
