@@ -18,7 +18,7 @@ TAU_S = 1e-5  # score tolerance relative to sum |w| |q.k| (bf16 operands, f32 ac
 def _workload(seed, L, H, d, raw=False, scale=1.0):
     from paper_2605_07363_b200 import IndexerWorkload
     K, Q, W = O.synthetic_prefill(seed, L, H, d, T=1, raw_gates=raw)
-    return IndexerWorkload(K, Q[0] * scale, W[0])
+    return IndexerWorkload(K, Q[0] * scale, W[0].astype(np.float32).astype(np.float64))  # f32 gates: exact on device
 
 
 def _near_tie_ok(got, exp, scores, mag, k):
