@@ -290,17 +290,16 @@ namespace misa {
 //   s0 += (w0, w1) * (relu x0, relu x1),  s1 += (w2, w3) * (relu x2, relu x3),
 // and a query's score is (s0.x + s0.y) + (s1.x + s1.y).
 //
-// ReLU: either FMNMX (ALU pipe) or, on the FMA pipe, y = x + |x| (one FADD2 for two heads:
-// exactly 2x for x >= 0 and +0 for x < 0) fed to the same FFMA2 — that accumulator then
-// holds exactly twice the FMNMX one (scaling by 2 commutes with rounding), and is halved
-// (exactly) before the final sums, so both forms give bit-identical scores.
-// MISA_RELU_FMA selects which accumulators use the FMA form: 0 none, 1 all, 2 (default) the second
-// of each pair (s1 / A[2], A[3]) — the ALU and FMA pipes then share the epilogue's ReLUs
-// (A/B at C4, tools/variant_lib.py: DSA filter 111.4 -> 105.5-107.3 ms, MISA filter
-// 14.9-15.1 -> 14.5-14.9, refine 26.6 -> 24-26; all-FMA form: MISA filter slower, 15.2-15.6).
-#ifndef MISA_RELU_FMA
-#define MISA_RELU_FMA 2
-#endif
+// ReLU runs half on the ALU pipe (FMNMX) and half on the FMA pipe: for the second pair of
+// each group of four heads (s1 here, A[2] / A[3] below) y = x + |x| (one FADD2 for two heads)
+// is exactly 2 relu(x), and those heads' gate weights are stored HALVED (exact), so
+// (w / 2) * y == w * relu(x) exactly and the fma chain is bit-identical to the all-FMNMX
+// form — the ALU and FMA pipes share the epilogue's ReLUs.  Callers pass w4 with .z / .w
+// (head slots 2, 3 of the group) already halved (gate_half_hi).  (A/B at C4,
+// tools/variant_lib.py: DSA filter 111.4 -> 105.5-107.3 ms, refine 26.6 -> 24-26; halving the
+// stored weights instead of the accumulators: MISA filter 15.2-15.4 -> 14.6-14.9; the
+// all-FMA form made the MISA filter slower, 15.2-15.6 vs 14.9-15.1; skipping empty ballots
+// in the filter's append loop made it slower too, 15.3 -> 15.5-16.0, coarse 15.6 -> 17.0-17.6.)
 __device__ __forceinline__ float2 relu2_alu(uint32_t x0, uint32_t x1) {
   return make_float2(fmaxf(__uint_as_float(x0), 0.f), fmaxf(__uint_as_float(x1), 0.f));
 }
@@ -308,40 +307,30 @@ __device__ __forceinline__ float2 relu2_fma_x2(uint32_t x0, uint32_t x1) {  // 2
   const float2 x = make_float2(__uint_as_float(x0), __uint_as_float(x1));
   return __fadd2_rn(x, make_float2(fabsf(x.x), fabsf(x.y)));
 }
-__device__ __forceinline__ float2 half2f(const float2 a) { return make_float2(0.5f * a.x, 0.5f * a.y); }
+// gate weight as stored for head slot j of a group of four: slots 2, 3 halved
+__device__ __forceinline__ float gate_stored(float w, int head_slot) { return (head_slot & 2) ? 0.5f * w : w; }
+__device__ __forceinline__ float4 gate_half_hi(float4 w) { return make_float4(w.x, w.y, 0.5f * w.z, 0.5f * w.w); }
 
 __device__ __forceinline__ void gate_relu4(float2& s0, float2& s1, const float4 w, uint32_t x0, uint32_t x1,
                                            uint32_t x2, uint32_t x3) {
-  // with MISA_RELU_FMA the FMA-form accumulators carry 2x (see gate_relu_finish)
-  s0 = __ffma2_rn(make_float2(w.x, w.y), MISA_RELU_FMA == 1 ? relu2_fma_x2(x0, x1) : relu2_alu(x0, x1), s0);
-  s1 = __ffma2_rn(make_float2(w.z, w.w), MISA_RELU_FMA >= 1 ? relu2_fma_x2(x2, x3) : relu2_alu(x2, x3), s1);
+  s0 = __ffma2_rn(make_float2(w.x, w.y), relu2_alu(x0, x1), s0);
+  s1 = __ffma2_rn(make_float2(w.z, w.w), relu2_fma_x2(x2, x3), s1);  // w.z, w.w halved
 }
 __device__ __forceinline__ float gate_relu_finish(float2 s0, float2 s1) {
-  if (MISA_RELU_FMA == 1) s0 = half2f(s0);
-  if (MISA_RELU_FMA >= 1) s1 = half2f(s1);
   return (s0.x + s0.y) + (s1.x + s1.y);
 }
 
 // The same reduction for two queries at once (HQ = 8, "pair" TMEM layout): v[4g + o],
-// v[4g + o + 1] are head g of queries (a, b); w[g] = (w_a[g], w_b[g]).  Packed
-// accumulator A_i holds heads (i, i + 4) of both queries, exactly the fma chains of
-// gate_relu4's s0.x / s0.y / s1.x / s1.y, so .x / .y are bit-identical to
+// v[4g + o + 1] are head g of queries (a, b); w[g] = (w_a[g], w_b[g]) as stored (halved for
+// g & 2).  Packed accumulator A_i holds heads (i, i + 4) of both queries, exactly the fma
+// chains of gate_relu4's s0.x / s0.y / s1.x / s1.y, so .x / .y are bit-identical to
 // gate_relu_finish of query a / b.
 __device__ __forceinline__ float2 gate_relu_pair8(const uint32_t* v, int o, const float2 (&w)[8]) {
   float2 A[4];
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
-    const bool fma_form = MISA_RELU_FMA == 1 || (MISA_RELU_FMA == 2 && (g & 3) >= 2);
-    const float2 x = fma_form ? relu2_fma_x2(v[4 * g + o], v[4 * g + o + 1]) : relu2_alu(v[4 * g + o], v[4 * g + o + 1]);
+    const float2 x = (g & 2) ? relu2_fma_x2(v[4 * g + o], v[4 * g + o + 1]) : relu2_alu(v[4 * g + o], v[4 * g + o + 1]);
     A[g & 3] = __ffma2_rn(w[g], x, g < 4 ? make_float2(0.f, 0.f) : A[g & 3]);
-  }
-  if (MISA_RELU_FMA >= 1) {
-    A[2] = half2f(A[2]);
-    A[3] = half2f(A[3]);
-  }
-  if (MISA_RELU_FMA == 1) {
-    A[0] = half2f(A[0]);
-    A[1] = half2f(A[1]);
   }
   return __fadd2_rn(__fadd2_rn(A[0], A[1]), __fadd2_rn(A[2], A[3]));
 }

@@ -358,7 +358,8 @@ __global__ void __launch_bounds__(kRefThreads, 1)
                 ptx::mbar_arrive(&tempty[acc]);
               }
 #pragma unroll
-              for (int jj = 0; jj < 32; jj += 4) gate_relu4(s0, s1, w4[(c + jj) / 4], r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
+              for (int jj = 0; jj < 32; jj += 4)
+                gate_relu4(s0, s1, gate_half_hi(w4[(c + jj) / 4]), r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
             }
           }
           if constexpr (N < 32) {
@@ -367,7 +368,8 @@ __global__ void __launch_bounds__(kRefThreads, 1)
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
 #pragma unroll
-            for (int jj = 0; jj < N; jj += 4) gate_relu4(s0, s1, w4[jj / 4], r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
+            for (int jj = 0; jj < N; jj += 4)
+              gate_relu4(s0, s1, gate_half_hi(w4[jj / 4]), r[jj], r[jj + 1], r[jj + 2], r[jj + 3]);
           }
           const float sc = gate_relu_finish(s0, s1);
           const int i = j * 128 + quad * 32 + lane;

@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(ScoreCfg<D, HQ>::NUM_THREADS, 1)
           const int head = a.heads ? a.heads[(int64_t)row * HQ + j] : (j < a.H ? j : -1);
           if (head >= 0) wv = a.w[(int64_t)row * a.Hp + head];
         }
-        sW[r] = wv;
+        sW[r] = gate_stored(wv, col_head<HQ>(r));  // head slots 2, 3 of each group of four halved
       }
       if (et < G) {
         const int row = row0 + et;
