@@ -74,7 +74,14 @@ def _config(a, world):
     """The workload config, identical in both arms (ours / --impl reference)."""
     return {"workload": _workload_name(a), "L": a.L, "T": a.L, "H": a.H, "h": a.h, "d": a.d, "B": a.B, "k": a.k,
             "parallelism": f"key-sharded x{world}" if world > 1 else "single device",
-            "l2": "inputs larger than L2 (queries 2 GiB); no explicit flush"}
+            "l2": _l2_note(a)}
+
+
+def _l2_note(a):
+    qb = a.L * a.H * a.d * 2
+    if qb > 126 * 2**20:
+        return f"inputs larger than L2 (queries {qb / 2**30:.2f} GiB read once per step); no explicit flush"
+    return f"queries {qb / 2**20:.0f} MiB fit the 126 MB L2: steps after the first may hit L2
 
 
 def _peaks():
