@@ -81,7 +81,7 @@ def _l2_note(a):
     qb = a.L * a.H * a.d * 2
     if qb > 126 * 2**20:
         return f"inputs larger than L2 (queries {qb / 2**30:.2f} GiB read once per step); no explicit flush"
-    return f"queries {qb / 2**20:.0f} MiB fit the 126 MB L2: steps after the first may hit L2
+    return f"queries {qb / 2**20:.0f} MiB fit the 126 MB L2: steps after the first may hit L2"
 
 
 def _peaks():
