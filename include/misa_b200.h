@@ -41,6 +41,7 @@
  *                         (workload.py:40-110 per workload; the reference loops over them)
  *   misa_relevance_dots   dsa.py:18-34       relevance_dots (raw per-query dot products)
  *   misa_pack_rows_f64    workload.py:202-254 load_workload payload (f64) -> device bf16 layouts
+ *   misa_sparse_attention (no reference counterpart: PAPER.md Eq. 3, the selection's consumer)
  */
 #ifndef MISA_B200_H_
 #define MISA_B200_H_
@@ -263,6 +264,16 @@ int misa_score_filter_split(const void* keys, int64_t n_keys, int head_dim, cons
                             const int32_t* prefix_len, int64_t n_rows, const int32_t* items,
                             const int32_t* item_tiles, const int32_t* item_tile0, int n_items, const float* tau,
                             uint64_t* cand, int cap, int32_t* cand_count, void* stream);
+
+/* The indexer's consumer (Eq. 3, Sparse MLA in MQA mode; outside the reference):
+ * out[t][h][0:dv] = sum_{s in topk[t]} softmax_s(scale * q[t][h] . kv[s]) * kv[s][0:dv], one
+ * latent row per token shared by all heads.  queries bf16 [n_rows][128][dqk] (heads padded
+ * to 128 rows), kv bf16 [n_keys][dqk], topk [n_rows][topk_ld] (each row's k slots: tokens
+ * first, -1 after), out f32 [n_rows][n_heads][dv].  dqk 128 (dv 64/128) or 256 (dv
+ * 128/256). */
+int misa_sparse_attention(const void* queries, int64_t n_rows, int n_heads, int head_dim_qk, const void* kv,
+                          int64_t n_keys, const int32_t* topk, int64_t topk_ld, int k, int head_dim_v, float scale,
+                          float* out, void* stream);
 
 /* Multi-GPU merge: n_parts local (score, index) top-k lists per row (parts[p][t][i], scores
  * aligned, -1 padded) -> global top-k ascending.  Same tie rule (score desc, index asc).

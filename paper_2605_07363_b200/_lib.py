@@ -64,6 +64,7 @@ SIGNATURES: dict[str, list] = {
     "misa_score_filter_split": [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _i32,
                                 _vp, _vp, _i32, _vp, _vp],
     "misa_sort_rows": [_vp, _i64, _vp, _i64, _i32, _vp],
+    "misa_sparse_attention": [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _i64, _i32, _i32, _f32, _vp, _vp],
     "misa_relevance_dots": [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _i64, _vp],
     "misa_pack_rows_f64": [_vp, _i64, _i32, _i64, _i64, _vp, _i32, _i64, _vp, _vp],
 }
