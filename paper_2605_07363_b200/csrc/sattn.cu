@@ -70,13 +70,10 @@ __device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint3
   return d;
 }
 
-#ifndef MISA_SATTN_SWAP
-#define MISA_SATTN_SWAP 0
-#endif
 // MN-major SW128 operand: LBO = stride between 64-wide N atoms, SBO = stride between 8-row K
-// groups (MISA_SATTN_SWAP exchanges them: a build-time probe of the field convention)
-constexpr uint32_t kLbo = MISA_SATTN_SWAP ? 1024u : 128u * 128u;
-constexpr uint32_t kSbo = MISA_SATTN_SWAP ? 128u * 128u : 1024u;
+// groups (probed on a B200: the swapped assignment fails tests/test_gpu_sparse_attention.py)
+constexpr uint32_t kLbo = 128u * 128u;
+constexpr uint32_t kSbo = 1024u;
 
 template <int DQK, int DV>
 __global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ CUtensorMap tmap_q, const SattnArgs a) {
