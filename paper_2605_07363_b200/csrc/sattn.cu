@@ -16,8 +16,8 @@
 // finds the row's count n with a binary search and walks ceil(n / 128) tiles; slots past n
 // in the last tile are zero-filled and masked to probability 0; a row with no token gets 0.
 //
-// Warps: 0 gather producer (+ Q TMA), 1 MMA issuer, 2-5 softmax / epilogue (thread = head,
-// TMEM lane quadrant = warp % 4).
+// Warps: 0-3 gather producers (warp 0 lane 0 also loads Q), 4 MMA issuer, 5-8 softmax /
+// epilogue (thread = head, TMEM lane quadrant = warp % 4).
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -40,7 +40,10 @@ struct SattnCfg {
   static constexpr int ATOM = 128 * 128;              // 128 rows x 64 bf16
   static constexpr int Q_BYTES = ATOM * (DQK / 64);
   static constexpr int KV_BYTES = ATOM * (DQK / 64);  // one 128-token tile
-  static constexpr int STAGES = DQK <= 128 ? 2 : 1;
+  static constexpr int STAGES = DQK <= 128 ? 4 : 1;
+  // independent gather warps (the gather rate scales with producer warps, tools/ubench_gather.cu);
+  // never more than stages (parity waits cannot tell ring rounds r and r + 2 apart)
+  static constexpr int GROUPS = STAGES;
   static constexpr int P_BYTES = 2 * ATOM;            // 128 heads x 128 tokens, K-major
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = OFF_Q + Q_BYTES;
@@ -75,8 +78,12 @@ __device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint3
 constexpr uint32_t kLbo = 128u * 128u;
 constexpr uint32_t kSbo = 1024u;
 
+constexpr int kSattnProd = 4;                             // producer warp slots
+constexpr int kSattnMma = kSattnProd;                     // MMA warp
+constexpr int kSattnThreads = 32 * (kSattnProd + 1 + 4);  // + 4 softmax warps
+
 template <int DQK, int DV>
-__global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ CUtensorMap tmap_q, const SattnArgs a) {
+__global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_constant__ CUtensorMap tmap_q, const SattnArgs a) {
   using C = SattnCfg<DQK>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -112,7 +119,7 @@ __global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ C
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmap_q);
     for (int i = 0; i < STAGES; ++i) {
-      ptx::mbar_init(&full[i], 32);
+      ptx::mbar_init(&full[i], 32);  // one producer warp fills a stage
       ptx::mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -127,18 +134,20 @@ __global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ C
     ptx::mbar_init(oempty, 128);
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == kSattnMma) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;  // S buffers at columns 0 / 128, O at 256
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ gather producer
-    int g = 0;  // tiles gathered so far (both passes): stage g % STAGES
+  if (warp < kSattnProd) {
+    // ------------------------------------------------------------ gather producers
+    // warp w gathers the CTA-global tiles g == w (mod GROUPS) of the (row, pass, tile) sequence
+    const int grp = warp;
+    int g = 0;  // tiles of the sequence so far (both passes): stage g % STAGES
     int rr = 0;
-    for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
-      if (lane == 0) {
+    for (int t = blockIdx.x; t < a.T && grp < C::GROUPS; t += gridDim.x, ++rr) {
+      if (grp == 0 && lane == 0) {
         ptx::mbar_wait(qempty, (rr & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(qfull, C::Q_BYTES);
 #pragma unroll
@@ -149,11 +158,13 @@ __global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ C
       const int nt = (n + 127) / 128;
       for (int pass = 0; pass < 2; ++pass) {
         for (int j = 0; j < nt; ++j, ++g) {
+          if (g % C::GROUPS != grp) continue;
           const int s = g % STAGES;
           ptx::mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
           uint8_t* stage = sKV + s * C::KV_BYTES;
           // the tile's tokens (clamped into the cache: the indexer only emits valid tokens)
-          __shared__ int sTok[128];
+          __shared__ int sTokAll[kSattnProd][128];
+          int* sTok = sTokAll[grp];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int i = j * 128 + 32 * u + lane;
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ C
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kSattnMma) {
     // ------------------------------------------------------------ MMA issuer
     if (ptx::elect_one()) {
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128);
@@ -242,44 +253,57 @@ __global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ C
           ptx::mbar_wait(&tfull[b], (sb >> 1) & 1);
           __syncwarp();
           ptx::tc_fence_after();
-          uint32_t x[128];
-#pragma unroll
-          for (int c = 0; c < 128; c += 32) ptx::tmem_ld_x32p(tmem_base + lane_off + b * 128 + c, x + c);
-#pragma unroll
-          for (int c = 0; c < 128; c += 32) ptx::tmem_wait_ld_dep32p(x + c);
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty[b]);
           const int nv = n - j * 128;  // valid columns of this tile
-          auto valid = [&](int c) { return c < nv; };
+          const uint32_t s_addr = tmem_base + lane_off + b * 128;
           if (pass == 0) {
-            float mx = m;
+            // running max / sum over the tile, 32 columns at a time
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+              uint32_t x[32];
+              ptx::tmem_ld_x32p(s_addr + c0, x);
+              ptx::tmem_wait_ld_dep32p(x);
+              if (c0 + 32 >= 128) {
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[b]);
+              }
+              float mx = m;
 #pragma unroll
-            for (int c = 0; c < 128; ++c)
-              if (valid(c)) mx = fmaxf(mx, __uint_as_float(x[c]) * a.scale_log2);
-            float acc = 0.f;
+              for (int c = 0; c < 32; ++c)
+                if (c0 + c < nv) mx = fmaxf(mx, __uint_as_float(x[c]) * a.scale_log2);
+              float acc = 0.f;
 #pragma unroll
-            for (int c = 0; c < 128; ++c)
-              if (valid(c)) acc += exp2f(__uint_as_float(x[c]) * a.scale_log2 - mx);
-            l = (m == -INFINITY ? 0.f : l * exp2f(m - mx)) + acc;
-            m = mx;
+              for (int c = 0; c < 32; ++c)
+                if (c0 + c < nv) acc += exp2f(__uint_as_float(x[c]) * a.scale_log2 - mx);
+              l = (m == -INFINITY ? 0.f : l * exp2f(m - mx)) + acc;
+              m = mx;
+            }
             continue;
           }
           const float inv_l = l > 0.f ? 1.f / l : 0.f;
           // P row (this head, 128 tokens) -> bf16 K-major SW128 (2 atoms of 64 tokens)
           ptx::mbar_wait(pempty, (np & 1) ^ 1);
           __syncwarp();
-#pragma unroll
-          for (int c = 0; c < 128; c += 8) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-              const float p0 = valid(c + e) ? exp2f(__uint_as_float(x[c + e]) * a.scale_log2 - m) * inv_l : 0.f;
-              const float p1 =
-                  valid(c + e + 1) ? exp2f(__uint_as_float(x[c + e + 1]) * a.scale_log2 - m) * inv_l : 0.f;
-              const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-              pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t x[32];
+            ptx::tmem_ld_x32p(s_addr + c0, x);
+            ptx::tmem_wait_ld_dep32p(x);
+            if (c0 + 32 >= 128) {
+              ptx::tc_fence_before();
+              ptx::mbar_arrive(&tempty[b]);
             }
-            *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, c, C::ATOM)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                const int cc = c0 + c + e;
+                const float p0 = cc < nv ? exp2f(__uint_as_float(x[c + e]) * a.scale_log2 - m) * inv_l : 0.f;
+                const float p1 = cc + 1 < nv ? exp2f(__uint_as_float(x[c + e + 1]) * a.scale_log2 - m) * inv_l : 0.f;
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+              }
+              *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, c0 + c, C::ATOM)) =
+                  make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
           }
           ptx::fence_proxy_async_smem();  // generic P writes -> the PV MMA's operand reads
           ptx::mbar_arrive(pfull);
@@ -311,7 +335,7 @@ __global__ void __launch_bounds__(192, 1) sattn_kernel(const __grid_constant__ C
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kSattnMma) {
     __syncwarp();
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, 512);
@@ -328,7 +352,7 @@ static int launch_sattn_t(const CUtensorMap& mq, const SattnArgs& a, cudaStream_
   auto kern = sattn_kernel<DQK, DV>;
   MISA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
   const int grid = a.T < sm_count() ? a.T : sm_count();
-  kern<<<grid, 192, C::SMEM_BYTES, st>>>(mq, a);
+  kern<<<grid, kSattnThreads, C::SMEM_BYTES, st>>>(mq, a);
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }
