@@ -9,9 +9,10 @@
 // resident for the row), the selected latent rows are gathered 128 at a time with 16-byte
 // cp.async into the 128-B-swizzled K-major tile (the refine kernel's gather), and the same
 // smem tile serves as K for S = Q K^T (K-major B) and as V for O += P V (the tile read
-// MN-major: rows = tokens = K, 64-dim row chunks = N).  Softmax is two-pass per row: pass 1
-// streams S tiles for the row max and sum, pass 2 recomputes S, writes P = exp(S - m) / l in
-// bf16 to shared memory (the K-major A operand) and accumulates O in TMEM — no O rescaling.
+// MN-major: rows = tokens = K, 64-dim row chunks = N).  Online softmax with a lazily raised
+// max: P = exp2(S - m) in bf16 to shared memory (the K-major A operand), O accumulated in
+// TMEM and rescaled in place only when a tile's max exceeds m by more than 2^8; O / l at the
+// end.  S is double-buffered in TMEM so the next tile's QK overlaps this tile's softmax.
 // A row's selected tokens come first, -1 padding after (the indexer's output): every role
 // finds the row's count n with a binary search and walks ceil(n / 128) tiles; slots past n
 // in the last tile are zero-filled and masked to probability 0; a row with no token gets 0.
@@ -82,6 +83,33 @@ constexpr int kSattnProd = 4;                             // producer warp slots
 constexpr int kSattnMma = kSattnProd;                     // MMA warp
 constexpr int kSattnThreads = 32 * (kSattnProd + 1 + 4);  // + 4 softmax warps
 
+// 32 lanes x 32 columns of 32 bits from registers into TMEM (the O rescale).
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 2^x with one MUFU.EX2 (P is rounded to bf16 right after: the approximation is far below that)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Online softmax: P is formed against a running max m that is only raised (and O rescaled
+// in TMEM) when a tile's max exceeds it by more than kLazy (log2 units) — exp2(x - m) then
+// stays <= 2^kLazy, exact enough in the bf16 P and the f32 accumulators, and the rescale is
+// rare after the first tiles.
+constexpr float kLazy = 8.f;
+
 template <int DQK, int DV>
 __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_constant__ CUtensorMap tmap_q, const SattnArgs a) {
   using C = SattnCfg<DQK>;
@@ -96,8 +124,8 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
   uint64_t* empty = bars + STAGES;        // [STAGES] MMAs done with the tile
   uint64_t* tfull = empty + STAGES;       // [2] S buffer computed
   uint64_t* tempty = tfull + 2;           // [2] S buffer read
-  uint64_t* pfull = tempty + 2;           // P written
-  uint64_t* pempty = pfull + 1;           // P consumed by the PV MMA
+  uint64_t* pfull = tempty + 2;           // P written (and O rescaled if needed)
+  uint64_t* pempty = pfull + 1;           // P consumed by the PV MMA (O is stable)
   uint64_t* qfull = pempty + 1;           // Q of the row landed
   uint64_t* qempty = qfull + 1;           // the row's MMAs are done with Q
   uint64_t* ofull = qempty + 1;           // O of the row complete
@@ -142,9 +170,9 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
 
   if (warp < kSattnProd) {
     // ------------------------------------------------------------ gather producers
-    // warp w gathers the CTA-global tiles g == w (mod GROUPS) of the (row, pass, tile) sequence
+    // warp w gathers the CTA-global tiles g == w (mod GROUPS) of the (row, tile) sequence
     const int grp = warp;
-    int g = 0;  // tiles of the sequence so far (both passes): stage g % STAGES
+    int g = 0;  // tiles of the sequence so far: stage g % STAGES
     int rr = 0;
     for (int t = blockIdx.x; t < a.T && grp < C::GROUPS; t += gridDim.x, ++rr) {
       if (grp == 0 && lane == 0) {
@@ -156,35 +184,33 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
       const int32_t* sel = a.topk + (int64_t)t * a.topk_ld;
       const int n = row_count(t);
       const int nt = (n + 127) / 128;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int j = 0; j < nt; ++j, ++g) {
-          if (g % C::GROUPS != grp) continue;
-          const int s = g % STAGES;
-          ptx::mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
-          uint8_t* stage = sKV + s * C::KV_BYTES;
-          // the tile's tokens (clamped into the cache: the indexer only emits valid tokens)
-          __shared__ int sTokAll[kSattnProd][128];
-          int* sTok = sTokAll[grp];
+      for (int j = 0; j < nt; ++j, ++g) {
+        if (g % C::GROUPS != grp) continue;
+        const int s = g % STAGES;
+        ptx::mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        uint8_t* stage = sKV + s * C::KV_BYTES;
+        // the tile's tokens (clamped into the cache: the indexer only emits valid tokens)
+        __shared__ int sTokAll[kSattnProd][128];
+        int* sTok = sTokAll[grp];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = j * 128 + 32 * u + lane;
-            const int v = i < n ? __ldg(sel + i) : -1;
-            sTok[32 * u + lane] = v < 0 ? -1 : (v < a.n_keys ? v : a.n_keys - 1);
-          }
-          __syncwarp();
-          // every instruction moves 32 consecutive 16-byte chunks: whole token rows, coalesced
-          constexpr int CH = DQK / 8;  // 16-byte chunks per token row
-#pragma unroll 4
-          for (int e = lane; e < 128 * CH; e += 32) {
-            const int r = e / CH, ch = e % CH;
-            const int ti = sTok[r];
-            const __nv_bfloat16* src = a.kv + (int64_t)(ti < 0 ? 0 : ti) * DQK + ch * 8;
-            sattn_cp16(stage + ptx::sw128_offset(r, ch * 8, C::ATOM), src, ti < 0 ? 0u : 16u);
-          }
-          __syncwarp();  // sTok is rewritten by the next tile
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ptx::smem_u32(&full[s]))
-                       : "memory");
+        for (int u = 0; u < 4; ++u) {
+          const int i = j * 128 + 32 * u + lane;
+          const int v = i < n ? __ldg(sel + i) : -1;
+          sTok[32 * u + lane] = v < 0 ? -1 : (v < a.n_keys ? v : a.n_keys - 1);
         }
+        __syncwarp();
+        // every instruction moves 32 consecutive 16-byte chunks: whole token rows, coalesced
+        constexpr int CH = DQK / 8;  // 16-byte chunks per token row
+#pragma unroll 4
+        for (int e = lane; e < 128 * CH; e += 32) {
+          const int r = e / CH, ch = e % CH;
+          const int ti = sTok[r];
+          const __nv_bfloat16* src = a.kv + (int64_t)(ti < 0 ? 0 : ti) * DQK + ch * 8;
+          sattn_cp16(stage + ptx::sw128_offset(r, ch * 8, C::ATOM), src, ti < 0 ? 0u : 16u);
+        }
+        __syncwarp();  // sTok is rewritten by the next tile
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ptx::smem_u32(&full[s]))
+                     : "memory");
       }
     }
   } else if (warp == kSattnMma) {
@@ -192,46 +218,47 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     if (ptx::elect_one()) {
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, DV) | (1u << 16);  // B (V) read MN-major
-      int g = 0, sb = 0, rr = 0, npm = 0;  // gathered tiles, S buffers, rows, P tiles consumed
+      int g = 0, rr = 0;
       const uint32_t q_base = ptx::smem_u32(sQ), p_base = ptx::smem_u32(sP);
       const uint32_t o_tmem = tmem_base + 256;
+      auto issue_qk = [&](int gg) {  // S[gg & 1] = Q K_gg^T
+        const int s = gg % STAGES, b = gg & 1;
+        const uint32_t kv_base = ptx::smem_u32(sKV + s * C::KV_BYTES);
+        ptx::mbar_wait(&tempty[b], ((gg >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&full[s], (gg / STAGES) & 1);
+        ptx::fence_proxy_async_smem();  // cp.async writes -> tensor-core reads
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DQK / 16; ++kk) {
+          const uint32_t koff = (kk & 3) * 32;
+          ptx::mma_bf16(tmem_base + b * 128, ptx::sw128_kmajor_desc(q_base + (kk >> 2) * C::ATOM + koff),
+                        ptx::sw128_kmajor_desc(kv_base + (kk >> 2) * C::ATOM + koff), idesc_s, kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(&tfull[b]);
+      };
       for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
         const int nt = (row_count(t) + 127) / 128;
         ptx::mbar_wait(qfull, rr & 1);
         ptx::tc_fence_after();
-        for (int pass = 0; pass < 2; ++pass) {
-          for (int j = 0; j < nt; ++j, ++g, ++sb) {
-            const int s = g % STAGES, b = sb & 1;
-            const uint32_t kv_base = ptx::smem_u32(sKV + s * C::KV_BYTES);
-            ptx::mbar_wait(&tempty[b], ((sb >> 1) & 1) ^ 1);
-            ptx::mbar_wait(&full[s], (g / STAGES) & 1);
-            ptx::fence_proxy_async_smem();  // cp.async writes -> tensor-core reads
-            ptx::tc_fence_after();
+        if (nt > 0) issue_qk(g);
+        for (int j = 0; j < nt; ++j, ++g) {
+          // the next S overlaps this tile's softmax (with one stage the next tile's gather needs
+          // this tile's PV done first: it is issued after it)
+          if (STAGES > 1 && j + 1 < nt) issue_qk(g + 1);
+          const int s = g % STAGES;
+          const uint32_t kv_base = ptx::smem_u32(sKV + s * C::KV_BYTES);
+          if (j == 0) ptx::mbar_wait(oempty, (rr & 1) ^ 1);  // the previous row's O was read
+          ptx::mbar_wait(pfull, g & 1);
+          ptx::tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < DQK / 16; ++kk) {
-              const uint32_t koff = (kk & 3) * 32;
-              ptx::mma_bf16(tmem_base + b * 128, ptx::sw128_kmajor_desc(q_base + (kk >> 2) * C::ATOM + koff),
-                            ptx::sw128_kmajor_desc(kv_base + (kk >> 2) * C::ATOM + koff), idesc_s, kk > 0 ? 1u : 0u);
-            }
-            ptx::mma_commit(&tfull[b]);
-            if (pass == 0) {
-              ptx::mma_commit(&empty[s]);
-              continue;
-            }
-            if (j == 0) ptx::mbar_wait(oempty, (rr & 1) ^ 1);  // the previous row's O was read
-            ptx::mbar_wait(pfull, npm & 1);
-            ++npm;
-            ptx::tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < 128 / 16; ++kk) {  // K = this tile's 128 tokens
-              const uint32_t koff = (kk & 3) * 32;
-              ptx::mma_bf16(o_tmem, ptx::sw128_kmajor_desc(p_base + (kk >> 2) * C::ATOM + koff),
-                            sw128_mnmajor_desc(kv_base + kk * 2048, kLbo, kSbo), idesc_o,
-                            (j > 0 || kk > 0) ? 1u : 0u);
-            }
-            ptx::mma_commit(&empty[s]);
-            ptx::mma_commit(pempty);
+          for (int kk = 0; kk < 128 / 16; ++kk) {  // K = this tile's 128 tokens
+            const uint32_t koff = (kk & 3) * 32;
+            ptx::mma_bf16(o_tmem, ptx::sw128_kmajor_desc(p_base + (kk >> 2) * C::ATOM + koff),
+                          sw128_mnmajor_desc(kv_base + kk * 2048, kLbo, kSbo), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           }
+          ptx::mma_commit(&empty[s]);
+          ptx::mma_commit(pempty);
+          if (STAGES == 1 && j + 1 < nt) issue_qk(g + 1);
         }
         ptx::mma_commit(ofull);
         ptx::mma_commit(qempty);
@@ -242,90 +269,94 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     const int quad = warp & 3;
     const int head = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    int g = 0, sb = 0, np = 0, rr = 0;
+    const uint32_t o_addr = tmem_base + lane_off + 256;
+    int g = 0, rr = 0;
     for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
       const int n = row_count(t);
       const int nt = (n + 127) / 128;
-      float m = -INFINITY, l = 0.f;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int j = 0; j < nt; ++j, ++g, ++sb) {
-          const int b = sb & 1;
-          ptx::mbar_wait(&tfull[b], (sb >> 1) & 1);
-          __syncwarp();
-          ptx::tc_fence_after();
-          const int nv = n - j * 128;  // valid columns of this tile
-          const uint32_t s_addr = tmem_base + lane_off + b * 128;
-          if (pass == 0) {
-            // running max / sum over the tile, 32 columns at a time
-            for (int c0 = 0; c0 < 128; c0 += 32) {
-              uint32_t x[32];
-              ptx::tmem_ld_x32p(s_addr + c0, x);
-              ptx::tmem_wait_ld_dep32p(x);
-              if (c0 + 32 >= 128) {
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&tempty[b]);
-              }
-              float mx = m;
+      float m = -INFINITY, l = 0.f;  // running (lazy) max in log2 units, sum of P
+      for (int j = 0; j < nt; ++j, ++g) {
+        const int b = g & 1;
+        const int nv = n - j * 128;  // valid columns of this tile
+        const uint32_t s_addr = tmem_base + lane_off + b * 128;
+        ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
+        __syncwarp();
+        ptx::tc_fence_after();
+        float mt = -INFINITY;  // this tile's max (log2 units), S read 32 columns at a time
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t x[32];
+          ptx::tmem_ld_x32p(s_addr + c0, x);
+          ptx::tmem_wait_ld_dep32p(x);
 #pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (c0 + c < nv) mx = fmaxf(mx, __uint_as_float(x[c]) * a.scale_log2);
-              float acc = 0.f;
-#pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (c0 + c < nv) acc += exp2f(__uint_as_float(x[c]) * a.scale_log2 - mx);
-              l = (m == -INFINITY ? 0.f : l * exp2f(m - mx)) + acc;
-              m = mx;
-            }
-            continue;
-          }
-          const float inv_l = l > 0.f ? 1.f / l : 0.f;
-          // P row (this head, 128 tokens) -> bf16 K-major SW128 (2 atoms of 64 tokens)
-          ptx::mbar_wait(pempty, (np & 1) ^ 1);
-          __syncwarp();
-          for (int c0 = 0; c0 < 128; c0 += 32) {
-            uint32_t x[32];
-            ptx::tmem_ld_x32p(s_addr + c0, x);
-            ptx::tmem_wait_ld_dep32p(x);
-            if (c0 + 32 >= 128) {
-              ptx::tc_fence_before();
-              ptx::mbar_arrive(&tempty[b]);
-            }
-#pragma unroll
-            for (int c = 0; c < 32; c += 8) {
-              uint32_t pk[4];
-#pragma unroll
-              for (int e = 0; e < 8; e += 2) {
-                const int cc = c0 + c + e;
-                const float p0 = cc < nv ? exp2f(__uint_as_float(x[c + e]) * a.scale_log2 - m) * inv_l : 0.f;
-                const float p1 = cc + 1 < nv ? exp2f(__uint_as_float(x[c + e + 1]) * a.scale_log2 - m) * inv_l : 0.f;
-                const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-              }
-              *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, c0 + c, C::ATOM)) =
-                  make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
-          }
-          ptx::fence_proxy_async_smem();  // generic P writes -> the PV MMA's operand reads
-          ptx::mbar_arrive(pfull);
-          ++np;
+          for (int c = 0; c < 32; ++c)
+            if (c0 + c < nv) mt = fmaxf(mt, __uint_as_float(x[c]));
         }
+        mt = mt * a.scale_log2;  // scale > 0: the max of the scaled scores
+        // P of the previous tile consumed: O is stable and sP free
+        ptx::mbar_wait(pempty, (g & 1) ^ 1);
+        __syncwarp();
+        if (mt > m + kLazy) {  // raise the max; rescale O and l (not before the first tile)
+          const float alpha = fast_exp2(m - mt);
+          l *= alpha;
+          if (j > 0) {
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < DV; c += 32) {
+              uint32_t o[32];
+              ptx::tmem_ld_x32p(o_addr + c, o);
+              ptx::tmem_wait_ld_dep32p(o);
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st_x32(o_addr + c, o);
+            }
+            tmem_wait_st();
+          }
+          m = mt;
+        }
+        // P row (this head, 128 tokens) -> bf16 K-major SW128 (2 atoms of 64 tokens); S re-read
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t x[32];
+          ptx::tmem_ld_x32p(s_addr + c0, x);
+          ptx::tmem_wait_ld_dep32p(x);
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const int cc = c0 + c + e;
+              const float p0 = cc < nv ? fast_exp2(fmaf(__uint_as_float(x[c + e]), a.scale_log2, -m)) : 0.f;
+              const float p1 = cc + 1 < nv ? fast_exp2(fmaf(__uint_as_float(x[c + e + 1]), a.scale_log2, -m)) : 0.f;
+              const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+              l += __low2float(h2) + __high2float(h2);  // the sum of what PV actually weighs
+              pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, c0 + c, C::ATOM)) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[b]);  // S read twice (max, then P): the buffer can be refilled
+        ptx::fence_proxy_async_smem();  // generic P writes -> the PV MMA's operand reads
+        ptx::tc_fence_before();         // the O rescale (tcgen05.st) before the next MMA
+        ptx::mbar_arrive(pfull);
       }
-      // epilogue: O row of this head -> out[t][head][0:DV]
+      // epilogue: O row / l of this head -> out[t][head][0:DV]
       ptx::mbar_wait(ofull, rr & 1);
       __syncwarp();
       ptx::tc_fence_after();
+      const float inv_l = l > 0.f ? 1.f / l : 0.f;
       float* orow = a.out + ((int64_t)t * a.H + head) * DV;
 #pragma unroll
       for (int c = 0; c < DV; c += 32) {
         uint32_t o[32];
-        ptx::tmem_ld_x32p(tmem_base + lane_off + 256 + c, o);
+        ptx::tmem_ld_x32p(o_addr + c, o);
         ptx::tmem_wait_ld_dep32p(o);
         if (head < a.H) {  // a row without tokens: O was never written, its output is 0
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
             *reinterpret_cast<float4*>(orow + c + e) =
-                n > 0 ? make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]), __uint_as_float(o[e + 2]),
-                                    __uint_as_float(o[e + 3]))
+                n > 0 ? make_float4(__uint_as_float(o[e]) * inv_l, __uint_as_float(o[e + 1]) * inv_l,
+                                    __uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l)
                       : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
@@ -369,6 +400,7 @@ extern "C" int misa_sparse_attention(const void* queries, int64_t n_rows, int n_
   MISA_REQUIRE((reinterpret_cast<uintptr_t>(queries) & 15) == 0 && (reinterpret_cast<uintptr_t>(kv) & 15) == 0,
                "queries / kv must be 16-byte aligned");
   MISA_REQUIRE(n_keys < (int64_t(1) << 31) && n_rows < (int64_t(1) << 31), "too many rows / keys");
+  MISA_REQUIRE(scale > 0.f, "scale must be positive");
   CUtensorMap mq;
   const int rc = make_tmap_bf16_2d(&mq, queries, head_dim_qk, (uint64_t)n_rows * 128, head_dim_qk, 128);
   if (rc) return rc;
