@@ -17,8 +17,8 @@
 // finds the row's count n with a binary search and walks ceil(n / 128) tiles; slots past n
 // in the last tile are zero-filled and masked to probability 0; a row with no token gets 0.
 //
-// Warps: 0-3 gather producers (warp 0 lane 0 also loads Q), 4 MMA issuer, 5-8 softmax /
-// epilogue (thread = head, TMEM lane quadrant = warp % 4).
+// Warps: 0-3 gather producers (warp 0 lane 0 also loads Q), 4 MMA issuer, 5-12 softmax /
+// epilogue (thread = head and half of its columns, TMEM lane quadrant = warp % 4).
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -81,7 +81,8 @@ constexpr uint32_t kSbo = 1024u;
 
 constexpr int kSattnProd = 4;                             // producer warp slots
 constexpr int kSattnMma = kSattnProd;                     // MMA warp
-constexpr int kSattnThreads = 32 * (kSattnProd + 1 + 4);  // + 4 softmax warps
+constexpr int kSattnSoft0 = kSattnMma + 1;                // first of 8 softmax warps
+constexpr int kSattnThreads = 32 * (kSattnSoft0 + 8);
 
 // 32 lanes x 32 columns of 32 bits from registers into TMEM (the O rescale).
 __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
@@ -152,14 +153,14 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 128);
+      ptx::mbar_init(&tempty[i], 256);
     }
-    ptx::mbar_init(pfull, 128);
+    ptx::mbar_init(pfull, 256);
     ptx::mbar_init(pempty, 1);
     ptx::mbar_init(qfull, 1);
     ptx::mbar_init(qempty, 1);
     ptx::mbar_init(ofull, 1);
-    ptx::mbar_init(oempty, 128);
+    ptx::mbar_init(oempty, 256);
     ptx::fence_mbar_init();
   }
   if (warp == kSattnMma) ptx::tmem_alloc(tmem_slot, 512);
@@ -266,24 +267,30 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
+    // two warps per TMEM lane quadrant: half h of a head's 128 tile columns (and of O's DV
+    // columns) each; the two partial maxima meet in shared memory once per tile
     const int quad = warp & 3;
+    const int half = (warp - kSattnSoft0) >> 2;
     const int head = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t o_addr = tmem_base + lane_off + 256;
+    constexpr int OH = DV / 2;  // O columns per half
+    __shared__ float sMax[2][2][128];  // [tile parity][half][head]
+    __shared__ float sL[2][128];
     int g = 0, rr = 0;
     for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
       const int n = row_count(t);
       const int nt = (n + 127) / 128;
-      float m = -INFINITY, l = 0.f;  // running (lazy) max in log2 units, sum of P
+      float m = -INFINITY, l = 0.f;  // running (lazy) max in log2 units, this half's sum of P
       for (int j = 0; j < nt; ++j, ++g) {
         const int b = g & 1;
-        const int nv = n - j * 128;  // valid columns of this tile
-        const uint32_t s_addr = tmem_base + lane_off + b * 128;
+        const int nv = n - j * 128 - half * 64;  // valid columns of this half-tile
+        const uint32_t s_addr = tmem_base + lane_off + b * 128 + half * 64;
         ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
         __syncwarp();
         ptx::tc_fence_after();
-        float mt = -INFINITY;  // this tile's max (log2 units), S read 32 columns at a time
-        for (int c0 = 0; c0 < 128; c0 += 32) {
+        float mt = -INFINITY;  // this half-tile's max, S read 32 columns at a time
+        for (int c0 = 0; c0 < 64; c0 += 32) {
           uint32_t x[32];
           ptx::tmem_ld_x32p(s_addr + c0, x);
           ptx::tmem_wait_ld_dep32p(x);
@@ -291,30 +298,32 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
           for (int c = 0; c < 32; ++c)
             if (c0 + c < nv) mt = fmaxf(mt, __uint_as_float(x[c]));
         }
-        mt = mt * a.scale_log2;  // scale > 0: the max of the scaled scores
+        sMax[b][half][head] = mt;
+        ptx::named_bar_sync(1, 256);
+        mt = fmaxf(sMax[b][0][head], sMax[b][1][head]) * a.scale_log2;  // scale > 0
         // P of the previous tile consumed: O is stable and sP free
         ptx::mbar_wait(pempty, (g & 1) ^ 1);
         __syncwarp();
-        if (mt > m + kLazy) {  // raise the max; rescale O and l (not before the first tile)
+        if (mt > m + kLazy) {  // raise the max; rescale this half of O and l (not on the first tile)
           const float alpha = fast_exp2(m - mt);
           l *= alpha;
           if (j > 0) {
             ptx::tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < DV; c += 32) {
+            for (int c = 0; c < OH; c += 32) {
               uint32_t o[32];
-              ptx::tmem_ld_x32p(o_addr + c, o);
+              ptx::tmem_ld_x32p(o_addr + half * OH + c, o);
               ptx::tmem_wait_ld_dep32p(o);
 #pragma unroll
               for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st_x32(o_addr + c, o);
+              tmem_st_x32(o_addr + half * OH + c, o);
             }
             tmem_wait_st();
           }
           m = mt;
         }
-        // P row (this head, 128 tokens) -> bf16 K-major SW128 (2 atoms of 64 tokens); S re-read
-        for (int c0 = 0; c0 < 128; c0 += 32) {
+        // P (this head, this half's 64 tokens = one SW128 atom) in bf16; S re-read
+        for (int c0 = 0; c0 < 64; c0 += 32) {
           uint32_t x[32];
           ptx::tmem_ld_x32p(s_addr + c0, x);
           ptx::tmem_wait_ld_dep32p(x);
@@ -330,7 +339,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
               l += __low2float(h2) + __high2float(h2);  // the sum of what PV actually weighs
               pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
             }
-            *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, c0 + c, C::ATOM)) =
+            *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, half * 64 + c0 + c, C::ATOM)) =
                 make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
@@ -340,16 +349,19 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
         ptx::tc_fence_before();         // the O rescale (tcgen05.st) before the next MMA
         ptx::mbar_arrive(pfull);
       }
-      // epilogue: O row / l of this head -> out[t][head][0:DV]
+      // epilogue: O row / l of this head (this half of its DV columns) -> out[t][head]
+      sL[half][head] = l;
+      ptx::named_bar_sync(1, 256);
+      const float lt = sL[0][head] + sL[1][head];
+      const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
       ptx::mbar_wait(ofull, rr & 1);
       __syncwarp();
       ptx::tc_fence_after();
-      const float inv_l = l > 0.f ? 1.f / l : 0.f;
-      float* orow = a.out + ((int64_t)t * a.H + head) * DV;
+      float* orow = a.out + ((int64_t)t * a.H + head) * DV + half * OH;
 #pragma unroll
-      for (int c = 0; c < DV; c += 32) {
+      for (int c = 0; c < OH; c += 32) {
         uint32_t o[32];
-        ptx::tmem_ld_x32p(o_addr + c, o);
+        ptx::tmem_ld_x32p(o_addr + half * OH + c, o);
         ptx::tmem_wait_ld_dep32p(o);
         if (head < a.H) {  // a row without tokens: O was never written, its output is 0
 #pragma unroll
@@ -362,6 +374,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(oempty);
+      ptx::named_bar_sync(1, 256);  // sL is rewritten by the next row
     }
   }
   ptx::tc_fence_before();
