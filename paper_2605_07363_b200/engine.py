@@ -28,6 +28,7 @@ densely, so the result never depends on the estimate.
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -1025,20 +1026,24 @@ class IndexerEngine:
                              candidates=cand, n_fallback_rows=nfb, candidate_runs=runs)
 
 
-_SHARED: dict = {}
+_SHARED = threading.local()
 
 
 def shared_engine(method: str, **kw) -> IndexerEngine:
-    """One engine per (method, parameters) for the single-query API (``dsa_select``,
-    ``misa_select``, ...): its workspace and work lists are reused across calls instead of
-    being rebuilt per query.  Small LRU; not for concurrent use from several threads."""
-    key = (method, tuple(sorted(kw.items())))
-    eng = _SHARED.pop(key, None)
+    """One engine per (method, parameters) and thread for the single-query API
+    (``dsa_select``, ``misa_select``, ...): its workspace and work lists are reused across
+    calls instead of being rebuilt per query.  Per-thread small LRU, so concurrent calls from
+    several threads stay independent (the reference functions are thread-safe)."""
+    cache = getattr(_SHARED, "engines", None)
+    if cache is None:
+        cache = _SHARED.engines = {}
+    key = (method, torch.cuda.current_device(), tuple(sorted(kw.items())))
+    eng = cache.pop(key, None)
     if eng is None:
         eng = IndexerEngine(method, **kw)
-        while len(_SHARED) >= 8:
-            _SHARED.pop(next(iter(_SHARED)))
-    _SHARED[key] = eng
+        while len(cache) >= 8:
+            cache.pop(next(iter(cache)))
+    cache[key] = eng
     return eng
 
 
