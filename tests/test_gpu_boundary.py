@@ -181,3 +181,29 @@ def test_precision_contract_on_reference_generators(golden_dir):
         recalls.append(len(set(got.tolist()) & set(ref.tolist())) / len(ref))
     print("bf16-device vs reference64 set recall:", [round(r, 4) for r in recalls])
     assert min(recalls) >= 0.99, recalls
+
+
+def test_corpus_edge_shapes(tmp_path):
+    """Tiny prefixes (L = 1, L < B, L not a multiple of 128), H < 8 (padded heads), d = 16 (padded
+    dims), k > L: the batched corpus call equals the single-query drop-in and the oracle."""
+    from paper_2605_07363_b200 import IndexerConfig, IndexerWorkload, make_indexer
+    from paper_2605_07363_b200.corpus import Corpus, save_corpus, select_corpus
+    rng = np.random.default_rng(3)
+    ws = []
+    for L in (1, 5, 130, 1500):
+        K = O.bf16_round(rng.standard_normal((L, 16)))
+        Q = O.bf16_round(rng.standard_normal((4, 16)))
+        W = O.softmax_rows(rng.standard_normal((1, 4)))[0].astype(np.float32).astype(np.float64)
+        ws.append(IndexerWorkload(K, Q, W))
+    c = Corpus(save_corpus(ws, tmp_path, names=[f"w{i}.bin" for i in range(len(ws))]))
+    batch = c.to_device(256)
+    assert batch.bf16_exact
+    for m, kw in (("dsa", {}), ("misa", dict(active_heads_h=2, block_size=256)),
+                  ("misa_hier", dict(active_heads_h=2, block_size=256, candidate_kprime=64))):
+        ind = make_indexer(m, budget_k=32, **kw)
+        res = select_corpus(ind, c, batch=batch)
+        for s, w in enumerate(ws):
+            single = ind.select(w).selection.indices.tolist()
+            assert res[s].selection.indices.tolist() == single, (m, s)
+            if m == "dsa":
+                assert single == O.dsa_select(w.keys, w.queries, w.gate_weights, 32, "fast32")["selection"].tolist()
