@@ -17,7 +17,7 @@
 // finds the row's count n with a binary search and walks ceil(n / 128) tiles; slots past n
 // in the last tile are zero-filled and masked to probability 0; a row with no token gets 0.
 //
-// Warps: 0-3 gather producers (warp 0 lane 0 also loads Q), 4 MMA issuer, 5-12 softmax /
+// Warps: 0-3 gather producers, 4 MMA issuer, 13 Q loader / L2 prefetcher, 5-12 softmax /
 // epilogue (thread = head and half of its columns, TMEM lane quadrant = warp % 4).
 #include "common.cuh"
 #include "ptx.cuh"
@@ -50,7 +50,7 @@ struct SattnCfg {
   static constexpr int OFF_KV = OFF_Q + Q_BYTES;
   static constexpr int OFF_P = OFF_KV + STAGES * KV_BYTES;
   static constexpr int OFF_BAR = OFF_P + P_BYTES;
-  static constexpr int NUM_BARS = 2 * STAGES + 4 + 2 + 2 + 2;
+  static constexpr int NUM_BARS = 2 * STAGES + 4 + 2 + 2 + 2 + 8;
   static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
@@ -82,7 +82,8 @@ constexpr uint32_t kSbo = 1024u;
 constexpr int kSattnProd = 4;                             // producer warp slots
 constexpr int kSattnMma = kSattnProd;                     // MMA warp
 constexpr int kSattnSoft0 = kSattnMma + 1;                // first of 8 softmax warps
-constexpr int kSattnThreads = 32 * (kSattnSoft0 + 8);
+constexpr int kSattnQ = kSattnSoft0 + 8;                  // Q loader (and L2 prefetch of the next row)
+constexpr int kSattnThreads = 32 * (kSattnQ + 1);
 
 // 32 lanes x 32 columns of 32 bits from registers into TMEM (the O rescale).
 __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
@@ -105,11 +106,45 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x for two values on the FMA pipe (x <= 126): Cody-Waite split x = i + f, |f| <= 1/2, by the
+// 1.5 * 2^23 rounding constant, 2^f by a cubic (least-squares fit on [-1/2, 1/2], relative
+// error 7.7e-5, far below P's bf16 rounding), 2^i added into the exponent bits.  A share of
+// P's exponentials runs here instead of on MUFU.EX2, whose 16 lanes per SM otherwise bound the
+// softmax (128 x 128 exponentials per tile = 1024 cycles, as long as the tile's two MMAs).
+#ifndef MISA_SATTN_EMU
+#define MISA_SATTN_EMU 0  // pairs of every four formed on the FMA pipe (A/B: 0 fastest)
+#endif
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  const float2 j = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = __fadd2_rn(j, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+  float2 q = __ffma2_rn(f, make_float2(0.05508868f, 0.05508868f), make_float2(0.24260405f, 0.24260405f));
+  q = __ffma2_rn(q, f, make_float2(0.6932762f, 0.6932762f));
+  q = __ffma2_rn(q, f, make_float2(0.99992895f, 0.99992895f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(j.y) << 23)));
+}
+
 // Online softmax: P is formed against a running max m that is only raised (and O rescaled
 // in TMEM) when a tile's max exceeds it by more than kLazy (log2 units) — exp2(x - m) then
 // stays <= 2^kLazy, exact enough in the bf16 P and the f32 accumulators, and the rescale is
 // rare after the first tiles.
 constexpr float kLazy = 8.f;
+
+#ifdef MISA_SATTN_TRACE
+// dev instrumentation (tools/sattn_trace.py): clock64 stamps of CTA 0's pipeline events
+constexpr int kTrEv = 16, kTrN = 1024;
+__device__ long long g_sattn_trace[kTrEv][kTrN];
+#define SATTN_TR(ev, idx)                                                                           \
+  do {                                                                                              \
+    if (blockIdx.x == 0 && (idx) < kTrN) g_sattn_trace[ev][idx] = clock64();                        \
+  } while (0)
+#else
+#define SATTN_TR(ev, idx) \
+  do {                    \
+  } while (0)
+#endif
 
 template <int DQK, int DV>
 __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_constant__ CUtensorMap tmap_q, const SattnArgs a) {
@@ -131,19 +166,27 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
   uint64_t* qempty = qfull + 1;           // the row's MMAs are done with Q
   uint64_t* ofull = qempty + 1;           // O of the row complete
   uint64_t* oempty = ofull + 1;           // O read by the epilogue
+  uint64_t* nfull = oempty + 1;           // [8] a row's token count published (ring by row)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // selected tokens of row t: the length of its non-negative prefix
+  // selected tokens of row t: the length of its non-negative prefix, warp-collective, in two
+  // dependent rounds (the last slot of each of 32 segments, then the first partial segment's
+  // slots) instead of a binary search's eleven; each warp role looks one row ahead, the MMA
+  // thread reads the count the Q loader publishes with the row's Q
   auto row_count = [&](int t) {
+    if (t >= a.T) return 0;
     const int32_t* sel = a.topk + (int64_t)t * a.topk_ld;
-    int lo = 0, hi = a.k;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(sel + mid) >= 0) lo = mid + 1;
-      else hi = mid;
-    }
-    return lo;
+    const int seg = (a.k + 31) / 32;
+    const bool full = lane * seg < a.k && __ldg(sel + min((lane + 1) * seg, a.k) - 1) >= 0;
+    const int base = __popc(__ballot_sync(~0u, full)) * seg;
+    int cnt = 0;
+    for (int i = lane; i < seg; i += 32) cnt += (base + i < a.k && __ldg(sel + base + i) >= 0) ? 1 : 0;
+    return min(base + (int)__reduce_add_sync(~0u, (unsigned)cnt), a.k);
   };
+  // row counts, Q loader -> MMA and softmax: a ring of 8 rows (the loader runs at most a few
+  // rows ahead: each of its Q loads waits for the previous row's QKs, which wait for the
+  // softmax of the tile before)
+  __shared__ int sRowN[8];
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmap_q);
@@ -161,6 +204,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     ptx::mbar_init(qempty, 1);
     ptx::mbar_init(ofull, 1);
     ptx::mbar_init(oempty, 256);
+    for (int i = 0; i < 8; ++i) ptx::mbar_init(&nfull[i], 1);
     ptx::fence_mbar_init();
   }
   if (warp == kSattnMma) ptx::tmem_alloc(tmem_slot, 512);
@@ -175,20 +219,17 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     const int grp = warp;
     int g = 0;  // tiles of the sequence so far: stage g % STAGES
     int rr = 0;
+    int n_nxt = grp < C::GROUPS ? row_count(blockIdx.x) : 0;
     for (int t = blockIdx.x; t < a.T && grp < C::GROUPS; t += gridDim.x, ++rr) {
-      if (grp == 0 && lane == 0) {
-        ptx::mbar_wait(qempty, (rr & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(qfull, C::Q_BYTES);
-#pragma unroll
-        for (int at = 0; at < DQK / 64; ++at) ptx::tma_load_2d(sQ + at * C::ATOM, &tmap_q, qfull, at * 64, t * 128);
-      }
       const int32_t* sel = a.topk + (int64_t)t * a.topk_ld;
-      const int n = row_count(t);
+      const int n = n_nxt;
+      n_nxt = row_count(t + gridDim.x);
       const int nt = (n + 127) / 128;
       for (int j = 0; j < nt; ++j, ++g) {
         if (g % C::GROUPS != grp) continue;
         const int s = g % STAGES;
         ptx::mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        if (lane == 0) SATTN_TR(0, g);
         uint8_t* stage = sKV + s * C::KV_BYTES;
         // the tile's tokens (clamped into the cache: the indexer only emits valid tokens)
         __shared__ int sTokAll[kSattnProd][128];
@@ -210,9 +251,43 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
           sattn_cp16(stage + ptx::sw128_offset(r, ch * 8, C::ATOM), src, ti < 0 ? 0u : 16u);
         }
         __syncwarp();  // sTok is rewritten by the next tile
+        if (lane == 0) SATTN_TR(1, g);
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ptx::smem_u32(&full[s]))
                      : "memory");
       }
+    }
+  } else if (warp == kSattnQ) {
+    // ------------------------------------------------------------ Q loader
+    // a row's Q lands as soon as the previous row's last QK is done; the next row's Q and
+    // selection are prefetched into L2 a row ahead so that neither that load nor the next row's
+    // index reads (its count, its tiles' token lists) go to HBM
+    int rr = 0;
+    int n_nxt = row_count(blockIdx.x);
+    for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
+      const int n = n_nxt;
+      n_nxt = row_count(t + gridDim.x);
+      const int tn = t + (int)gridDim.x;
+      if (tn < a.T) {
+        const char* seln = reinterpret_cast<const char*>(a.topk + (int64_t)tn * a.topk_ld);
+        for (int off = lane * 128; off < a.k * 4; off += 32 * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(seln + off));
+      }
+      if (lane == 0) {
+        sRowN[rr & 7] = n;
+        ptx::mbar_arrive(&nfull[rr & 7]);
+        ptx::mbar_wait(qempty, (rr & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(qfull, C::Q_BYTES);
+#pragma unroll
+        for (int at = 0; at < DQK / 64; ++at) ptx::tma_load_2d(sQ + at * C::ATOM, &tmap_q, qfull, at * 64, t * 128);
+        if (tn < a.T)
+          for (int at = 0; at < DQK / 64; ++at)
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tmap_q)),
+                         "r"(at * 64), "r"(tn * 128)
+                         : "memory");
+        SATTN_TR(9, rr);
+      }
+      __syncwarp();
     }
   } else if (warp == kSattnMma) {
     // ------------------------------------------------------------ MMA issuer
@@ -227,6 +302,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
         const uint32_t kv_base = ptx::smem_u32(sKV + s * C::KV_BYTES);
         ptx::mbar_wait(&tempty[b], ((gg >> 1) & 1) ^ 1);
         ptx::mbar_wait(&full[s], (gg / STAGES) & 1);
+        SATTN_TR(2, gg);
         ptx::fence_proxy_async_smem();  // cp.async writes -> tensor-core reads
         ptx::tc_fence_after();
 #pragma unroll
@@ -238,18 +314,30 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
         ptx::mma_commit(&tfull[b]);
       };
       for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
-        const int nt = (row_count(t) + 127) / 128;
+        ptx::mbar_wait(&nfull[rr & 7], (rr >> 3) & 1);
+        const int nt = (sRowN[rr & 7] + 127) / 128;
         ptx::mbar_wait(qfull, rr & 1);
+        SATTN_TR(10, rr);
         ptx::tc_fence_after();
+        // sQ is released as soon as the row's last QK is done (its next Q load then overlaps the
+        // last tile's softmax, PV and the epilogue)
         if (nt > 0) issue_qk(g);
+        if (nt <= 1) ptx::mma_commit(qempty);
         for (int j = 0; j < nt; ++j, ++g) {
           // the next S overlaps this tile's softmax (with one stage the next tile's gather needs
           // this tile's PV done first: it is issued after it)
-          if (STAGES > 1 && j + 1 < nt) issue_qk(g + 1);
+          if (STAGES > 1 && j + 1 < nt) {
+            issue_qk(g + 1);
+            if (j + 2 == nt) ptx::mma_commit(qempty);
+          }
           const int s = g % STAGES;
           const uint32_t kv_base = ptx::smem_u32(sKV + s * C::KV_BYTES);
-          if (j == 0) ptx::mbar_wait(oempty, (rr & 1) ^ 1);  // the previous row's O was read
+          if (j == 0) {
+            ptx::mbar_wait(oempty, (rr & 1) ^ 1);  // the previous row's O was read
+            SATTN_TR(13, rr);
+          }
           ptx::mbar_wait(pfull, g & 1);
+          SATTN_TR(3, g);
           ptx::tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 128 / 16; ++kk) {  // K = this tile's 128 tokens
@@ -259,10 +347,12 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
           }
           ptx::mma_commit(&empty[s]);
           ptx::mma_commit(pempty);
-          if (STAGES == 1 && j + 1 < nt) issue_qk(g + 1);
+          if (STAGES == 1 && j + 1 < nt) {
+            issue_qk(g + 1);
+            if (j + 2 == nt) ptx::mma_commit(qempty);
+          }
         }
         ptx::mma_commit(ofull);
-        ptx::mma_commit(qempty);
       }
     }
   } else {
@@ -277,16 +367,21 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     constexpr int OH = DV / 2;  // O columns per half
     __shared__ float sMax[2][2][128];  // [tile parity][half][head]
     __shared__ float sL[2][128];
+    const float sl = a.scale_log2;
+    const float2 sl2 = make_float2(sl, sl);
     int g = 0, rr = 0;
     for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
-      const int n = row_count(t);
+      ptx::mbar_wait(&nfull[rr & 7], (rr >> 3) & 1);
+      const int n = sRowN[rr & 7];
       const int nt = (n + 127) / 128;
-      float m = -INFINITY, l = 0.f;  // running (lazy) max in log2 units, this half's sum of P
+      float m = -INFINITY;               // running (lazy) max in log2 units
+      float2 l2 = make_float2(0.f, 0.f);  // this half's sum of P (two lanes of columns)
       for (int j = 0; j < nt; ++j, ++g) {
         const int b = g & 1;
         const int nv = n - j * 128 - half * 64;  // valid columns of this half-tile
         const uint32_t s_addr = tmem_base + lane_off + b * 128 + half * 64;
         ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
+        if (warp == kSattnSoft0 && lane == 0) SATTN_TR(4, g);
         __syncwarp();
         ptx::tc_fence_after();
         float mt = -INFINITY;  // this half-tile's max, S read 32 columns at a time
@@ -294,19 +389,28 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
           uint32_t x[32];
           ptx::tmem_ld_x32p(s_addr + c0, x);
           ptx::tmem_wait_ld_dep32p(x);
+          if (nv >= c0 + 32) {  // full chunk (all but a row's last tile): no per-column masks
+            float m2[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c0 + c < nv) mt = fmaxf(mt, __uint_as_float(x[c]));
+            for (int c = 0; c < 32; ++c) m2[c & 3] = fmaxf(m2[c & 3], __uint_as_float(x[c]));
+            mt = fmaxf(mt, fmaxf(fmaxf(m2[0], m2[1]), fmaxf(m2[2], m2[3])));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (c0 + c < nv) mt = fmaxf(mt, __uint_as_float(x[c]));
+          }
         }
         sMax[b][half][head] = mt;
         ptx::named_bar_sync(1, 256);
-        mt = fmaxf(sMax[b][0][head], sMax[b][1][head]) * a.scale_log2;  // scale > 0
+        mt = fmaxf(sMax[b][0][head], sMax[b][1][head]) * sl;  // scale > 0
+        if (warp == kSattnSoft0 && lane == 0) SATTN_TR(5, g);
         // P of the previous tile consumed: O is stable and sP free
         ptx::mbar_wait(pempty, (g & 1) ^ 1);
+        if (warp == kSattnSoft0 && lane == 0) SATTN_TR(7, g);
         __syncwarp();
         if (mt > m + kLazy) {  // raise the max; rescale this half of O and l (not on the first tile)
           const float alpha = fast_exp2(m - mt);
-          l *= alpha;
+          l2 = __fmul2_rn(l2, make_float2(alpha, alpha));
           if (j > 0) {
             ptx::tc_fence_after();
 #pragma unroll
@@ -322,58 +426,96 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
           }
           m = mt;
         }
-        // P (this head, this half's 64 tokens = one SW128 atom) in bf16; S re-read
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t x[32];
-          ptx::tmem_ld_x32p(s_addr + c0, x);
-          ptx::tmem_wait_ld_dep32p(x);
+        // P (this head, this half's 64 tokens = one SW128 atom) in bf16 from a second read of S:
+        // packed f32x2 scale-and-shift and sum; l sums the unrounded P (as flash attention does)
+        {
+          const float2 nm2 = make_float2(-m, -m);
 #pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            uint32_t pk[4];
+          for (int c0 = 0; c0 < 64; c0 += 32) {
+            uint32_t x[32];
+            ptx::tmem_ld_x32p(s_addr + c0, x);
+            ptx::tmem_wait_ld_dep32p(x);
+            const bool full_chunk = nv >= c0 + 32;
 #pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-              const int cc = c0 + c + e;
-              const float p0 = cc < nv ? fast_exp2(fmaf(__uint_as_float(x[c + e]), a.scale_log2, -m)) : 0.f;
-              const float p1 = cc + 1 < nv ? fast_exp2(fmaf(__uint_as_float(x[c + e + 1]), a.scale_log2, -m)) : 0.f;
-              const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-              l += __low2float(h2) + __high2float(h2);  // the sum of what PV actually weighs
-              pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+            for (int c = 0; c < 32; c += 8) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                const float2 y = __ffma2_rn(make_float2(__uint_as_float(x[c + e]), __uint_as_float(x[c + e + 1])),
+                                            sl2, nm2);
+                float p0, p1;
+                if ((e >> 1) < MISA_SATTN_EMU) {
+                  const float2 q = exp2_fma2(y);
+                  p0 = q.x, p1 = q.y;
+                } else {
+                  p0 = fast_exp2(y.x), p1 = fast_exp2(y.y);
+                }
+                if (!full_chunk) {
+                  p0 = c0 + c + e < nv ? p0 : 0.f;
+                  p1 = c0 + c + e + 1 < nv ? p1 : 0.f;
+                }
+                l2 = __fadd2_rn(l2, make_float2(p0, p1));
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+              }
+              *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, half * 64 + c0 + c, C::ATOM)) =
+                  make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
-            *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, half * 64 + c0 + c, C::ATOM)) =
-                make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[b]);  // S read twice (max, then P): the buffer can be refilled
+        if (warp == kSattnSoft0 && lane == 0) SATTN_TR(6, g);
         ptx::fence_proxy_async_smem();  // generic P writes -> the PV MMA's operand reads
         ptx::tc_fence_before();         // the O rescale (tcgen05.st) before the next MMA
         ptx::mbar_arrive(pfull);
+        if (warp == kSattnSoft0 && lane == 0) SATTN_TR(8, g);
       }
       // epilogue: O row / l of this head (this half of its DV columns) -> out[t][head]
-      sL[half][head] = l;
+      sL[half][head] = l2.x + l2.y;
       ptx::named_bar_sync(1, 256);
       const float lt = sL[0][head] + sL[1][head];
       const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
       ptx::mbar_wait(ofull, rr & 1);
+      if (warp == kSattnSoft0 && lane == 0) SATTN_TR(11, rr);
       __syncwarp();
       ptx::tc_fence_after();
-      float* orow = a.out + ((int64_t)t * a.H + head) * DV + half * OH;
+      // O / l through this warp's 4 KB of sP (free: the row's PVs are complete) — 32 heads x 32
+      // columns, 16-byte chunks XOR-swizzled by row — so each global store writes four whole
+      // 128-byte row segments instead of 32 scattered 16-byte pieces
+      uint8_t* stg = sP + (warp - kSattnSoft0) * 4096;
+      const uint32_t stg_a = ptx::smem_u32(stg);
 #pragma unroll
       for (int c = 0; c < OH; c += 32) {
         uint32_t o[32];
         ptx::tmem_ld_x32p(o_addr + half * OH + c, o);
         ptx::tmem_wait_ld_dep32p(o);
-        if (head < a.H) {  // a row without tokens: O was never written, its output is 0
+        const float f = n > 0 ? inv_l : 0.f;  // a row without tokens: O was never written, its output is 0
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(orow + c + e) =
-                n > 0 ? make_float4(__uint_as_float(o[e]) * inv_l, __uint_as_float(o[e + 1]) * inv_l,
-                                    __uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 v = make_float4(__uint_as_float(o[4 * c4]) * f, __uint_as_float(o[4 * c4 + 1]) * f,
+                                       __uint_as_float(o[4 * c4 + 2]) * f, __uint_as_float(o[4 * c4 + 3]) * f);
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg_a + (lane * 8 + (c4 ^ (lane & 7))) * 16),
+                       "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                       : "memory");
         }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 4 + (lane >> 3), c4 = lane & 7;
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "r"(stg_a + (r * 8 + (c4 ^ (r & 7))) * 16)
+                       : "memory");
+          const int hr = quad * 32 + r;
+          if (hr < a.H) *reinterpret_cast<float4*>(a.out + ((int64_t)t * a.H + hr) * DV + half * OH + c + c4 * 4) = v;
+        }
+        __syncwarp();  // the staging tile is rewritten by the next chunk
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(oempty);
+      if (warp == kSattnSoft0 && lane == 0) SATTN_TR(12, rr);
       ptx::named_bar_sync(1, 256);  // sL is rewritten by the next row
     }
   }
@@ -400,6 +542,12 @@ static int launch_sattn_t(const CUtensorMap& mq, const SattnArgs& a, cudaStream_
   MISA_LAUNCH_CHECK();
   return MISA_OK;
 }
+
+#ifdef MISA_SATTN_TRACE
+extern "C" int misa_sattn_trace_copy(long long* host) {
+  return cudaMemcpyFromSymbol(host, g_sattn_trace, sizeof(g_sattn_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" int misa_sparse_attention(const void* queries, int64_t n_rows, int n_heads, int head_dim_qk,
                                      const void* kv, int64_t n_keys, const int32_t* topk, int64_t topk_ld, int k,
