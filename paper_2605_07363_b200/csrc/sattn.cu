@@ -108,11 +108,13 @@ __device__ __forceinline__ float fast_exp2(float x) {
 
 // 2^x for two values on the FMA pipe (x <= 126): Cody-Waite split x = i + f, |f| <= 1/2, by the
 // 1.5 * 2^23 rounding constant, 2^f by a cubic (least-squares fit on [-1/2, 1/2], relative
-// error 7.7e-5, far below P's bf16 rounding), 2^i added into the exponent bits.  A share of
-// P's exponentials runs here instead of on MUFU.EX2, whose 16 lanes per SM otherwise bound the
-// softmax (128 x 128 exponentials per tile = 1024 cycles, as long as the tile's two MMAs).
+// error 7.7e-5, far below P's bf16 rounding), 2^i added into the exponent bits — an option to
+// move a share of P's exponentials off MUFU.EX2.  Measured at the C4 shape it does not pay:
+// the softmax is latency- not MUFU-bound (tools/sattn_trace.py: ~1.4k of a tile's ~2.5k cycles
+// in the P phase, XU pipe ~27% busy): 1 pair in 4 -> +0.6 ms, 2 in 4 -> +1.6 ms; MUFU.EX2 on
+// f16x2 pairs (half the MUFU ops) +1.2 ms; loading both S chunks before one wait +0.3 ms.
 #ifndef MISA_SATTN_EMU
-#define MISA_SATTN_EMU 0  // pairs of every four formed on the FMA pipe (A/B: 0 fastest)
+#define MISA_SATTN_EMU 0  // pairs of every four formed on the FMA pipe (0: none, the fastest)
 #endif
 __device__ __forceinline__ float2 exp2_fma2(float2 x) {
   x = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
@@ -384,20 +386,24 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
         if (warp == kSattnSoft0 && lane == 0) SATTN_TR(4, g);
         __syncwarp();
         ptx::tc_fence_after();
-        float mt = -INFINITY;  // this half-tile's max, S read 32 columns at a time
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t x[32];
-          ptx::tmem_ld_x32p(s_addr + c0, x);
+        float mt = -INFINITY;  // this half-tile's max: both 32-column loads in flight at once
+        {
+          uint32_t x[32], y[32];
+          ptx::tmem_ld_x32p(s_addr, x);
+          ptx::tmem_ld_x32p(s_addr + 32, y);
           ptx::tmem_wait_ld_dep32p(x);
-          if (nv >= c0 + 32) {  // full chunk (all but a row's last tile): no per-column masks
+          ptx::tmem_wait_ld_dep32p(y);
+          if (nv >= 64) {  // full half-tile (all but a row's last tile): no per-column masks
             float m2[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int c = 0; c < 32; ++c) m2[c & 3] = fmaxf(m2[c & 3], __uint_as_float(x[c]));
-            mt = fmaxf(mt, fmaxf(fmaxf(m2[0], m2[1]), fmaxf(m2[2], m2[3])));
+            for (int c = 0; c < 32; ++c) m2[c & 3] = fmaxf(m2[c & 3], fmaxf(__uint_as_float(x[c]), __uint_as_float(y[c])));
+            mt = fmaxf(fmaxf(m2[0], m2[1]), fmaxf(m2[2], m2[3]));
           } else {
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (c0 + c < nv) mt = fmaxf(mt, __uint_as_float(x[c]));
+            for (int c = 0; c < 32; ++c) {
+              if (c < nv) mt = fmaxf(mt, __uint_as_float(x[c]));
+              if (32 + c < nv) mt = fmaxf(mt, __uint_as_float(y[c]));
+            }
           }
         }
         sMax[b][half][head] = mt;
@@ -430,6 +436,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
         // packed f32x2 scale-and-shift and sum; l sums the unrounded P (as flash attention does)
         {
           const float2 nm2 = make_float2(-m, -m);
+          float2 lb2 = make_float2(0.f, 0.f);  // a second accumulator: two shorter FADD2 chains
 #pragma unroll
           for (int c0 = 0; c0 < 64; c0 += 32) {
             uint32_t x[32];
@@ -454,7 +461,8 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
                   p0 = c0 + c + e < nv ? p0 : 0.f;
                   p1 = c0 + c + e + 1 < nv ? p1 : 0.f;
                 }
-                l2 = __fadd2_rn(l2, make_float2(p0, p1));
+                if (e & 2) lb2 = __fadd2_rn(lb2, make_float2(p0, p1));
+                else l2 = __fadd2_rn(l2, make_float2(p0, p1));
                 const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                 pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
               }
@@ -462,6 +470,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
                   make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
           }
+          l2 = __fadd2_rn(l2, lb2);
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[b]);  // S read twice (max, then P): the buffer can be refilled
