@@ -60,6 +60,7 @@ def _args():
     p.add_argument("--no-hier", action="store_true", help="skip timing MISA-dagger (k'=--kprime)")
     p.add_argument("--hier", action="store_true", help=argparse.SUPPRESS)  # the default now
     p.add_argument("--no-needle", action="store_true", help="skip the needle-retrieval recall leg")
+    p.add_argument("--no-sattn", action="store_true", help="skip the sparse-attention consumer leg")
     p.add_argument("--no-decode", action="store_true", help="skip the C5 decode-step leg")
     p.add_argument("--no-sweep", action="store_true", help="skip the C2 / C3 prefill configs")
     p.add_argument("--no-c5", action="store_true", help="skip the C5 1M-key causal prefill leg")
@@ -517,6 +518,23 @@ def run_ours(a):
                           "eager engine.decode and CUDA-graph DecodeGraph replay, ms per step",
                   "rows": decode_numbers()}
 
+    # --- the selection's consumer: sparse attention over this layer's MISA top-k
+    sattn = None
+    if world == 1 and not a.no_sattn:
+        from paper_2605_07363_b200.sparse_attention import sparse_attention
+        gq = torch.Generator(device="cuda").manual_seed(1)
+        qa = torch.randn(T, 128, 128, device="cuda", generator=gq).bfloat16()
+        tk = res_m.topk
+        ms_sa = _time_steps(lambda: sparse_attention(qa, K, tk, 128), 3, 1, barrier)
+        n_sel = int((tk >= 0).sum().item())
+        fl = 2.0 * 2 * 128 * 128 * n_sel  # QK + PV over every selected token of every row
+        sattn = {"workload": f"MQA sparse attention over the MISA top-{a.k}: T={T} rows, 128 heads, "
+                             f"d_qk=d_v=128, latent rows = the layer's keys, bf16 in / f32 out",
+                 "ms": round(ms_sa, 3), "TFLOP_s": round(fl / ms_sa / 1e9, 1),
+                 "frac_tensor_burst": round(fl / ms_sa / 1e9 / tc_burst, 4)}
+        del qa
+        torch.cuda.empty_cache()
+
     c5 = None
     if world == 1 and not a.no_c5:
         del eng_m, eng_d, x
@@ -546,6 +564,7 @@ def run_ours(a):
         "fallback_rows": fallback,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         "decode": decode, "sharded_decode": sdec, "configs": sweep, "c5_prefill": c5, "needle": needle,
+        "sparse_attention": sattn,
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)
