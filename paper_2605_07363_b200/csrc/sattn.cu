@@ -81,10 +81,26 @@ constexpr uint32_t kSbo = 1024u;
 
 constexpr int kSattnProd = 4;                             // producer warp slots
 constexpr int kSattnMma = kSattnProd;                     // MMA warp
-constexpr int kSattnSoft0 = kSattnMma + 1;                // first of 8 softmax warps
-constexpr int kSattnQ = kSattnSoft0 + 8;                  // Q loader (and L2 prefetch of the next row)
+// Softmax warps per lane quadrant: 4 (16 warps of 32 columns, 80 registers, no spills) was
+// measured slower than 2 at the C4 shape (26.5 vs 24.8 ms: the 512-thread max exchange).
+#ifndef MISA_SATTN_SPLIT
+#define MISA_SATTN_SPLIT 2
+#endif
+constexpr int kSattnSplit = MISA_SATTN_SPLIT;             // softmax warps per TMEM lane quadrant
+static_assert(kSattnSplit == 2 || kSattnSplit == 4, "a head's 128 tile columns split in 2 or 4");
+constexpr int kSattnSoft0 = kSattnMma + 1;                // first softmax warp
+constexpr int kSattnSoftThreads = 128 * kSattnSplit;      // softmax / epilogue threads
+constexpr int kSattnQ = kSattnSoft0 + 4 * kSattnSplit;    // Q loader (and L2 prefetch of the next row)
 constexpr int kSattnThreads = 32 * (kSattnQ + 1);
 
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 // 32 lanes x 32 columns of 32 bits from registers into TMEM (the O rescale).
 __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -198,14 +214,14 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 256);
+      ptx::mbar_init(&tempty[i], kSattnSoftThreads);
     }
-    ptx::mbar_init(pfull, 256);
+    ptx::mbar_init(pfull, kSattnSoftThreads);
     ptx::mbar_init(pempty, 1);
     ptx::mbar_init(qfull, 1);
     ptx::mbar_init(qempty, 1);
     ptx::mbar_init(ofull, 1);
-    ptx::mbar_init(oempty, 256);
+    ptx::mbar_init(oempty, kSattnSoftThreads);
     for (int i = 0; i < 8; ++i) ptx::mbar_init(&nfull[i], 1);
     ptx::fence_mbar_init();
   }
@@ -359,86 +375,102 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
-    // two warps per TMEM lane quadrant: half h of a head's 128 tile columns (and of O's DV
-    // columns) each; the two partial maxima meet in shared memory once per tile
+    // kSattnSplit warps per TMEM lane quadrant: part p of a head's 128 tile columns (and of
+    // O's DV columns) each; the partial maxima meet in shared memory once per tile
+    constexpr int CW = 128 / kSattnSplit;  // tile columns per warp
+    constexpr int OP = DV / kSattnSplit;   // O columns per warp
+    constexpr int EC = C::P_BYTES / (4 * kSattnSplit) / (32 * 4);  // epilogue: staged columns per pass
+    constexpr int OC = OP < EC ? OP : EC;  // O columns per TMEM load / store (16 or 32)
     const int quad = warp & 3;
-    const int half = (warp - kSattnSoft0) >> 2;
+    const int part = (warp - kSattnSoft0) >> 2;
     const int head = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t o_addr = tmem_base + lane_off + 256;
-    constexpr int OH = DV / 2;  // O columns per half
-    __shared__ float sMax[2][2][128];  // [tile parity][half][head]
-    __shared__ float sL[2][128];
+    const uint32_t o_addr = tmem_base + lane_off + 256 + part * OP;
+    __shared__ float sMax[2][kSattnSplit][128];  // [tile parity][part][head]
+    __shared__ float sL[kSattnSplit][128];
     const float sl = a.scale_log2;
     const float2 sl2 = make_float2(sl, sl);
+    auto ld_o = [&](uint32_t addr, uint32_t* r) {
+      if constexpr (OC == 32) {
+        ptx::tmem_ld_x32p(addr, r);
+        ptx::tmem_wait_ld_dep32p(r);
+      } else {
+        ptx::tmem_ld_x16(addr, r);
+        ptx::tmem_wait_ld_dep16(r);
+      }
+    };
     int g = 0, rr = 0;
     for (int t = blockIdx.x; t < a.T; t += gridDim.x, ++rr) {
       ptx::mbar_wait(&nfull[rr & 7], (rr >> 3) & 1);
       const int n = sRowN[rr & 7];
       const int nt = (n + 127) / 128;
       float m = -INFINITY;               // running (lazy) max in log2 units
-      float2 l2 = make_float2(0.f, 0.f);  // this half's sum of P (two lanes of columns)
+      float2 l2 = make_float2(0.f, 0.f);  // this part's sum of P (two lanes of columns)
       for (int j = 0; j < nt; ++j, ++g) {
         const int b = g & 1;
-        const int nv = n - j * 128 - half * 64;  // valid columns of this half-tile
-        const uint32_t s_addr = tmem_base + lane_off + b * 128 + half * 64;
+        const int nv = n - j * 128 - part * CW;  // valid columns of this part of the tile
+        const uint32_t s_addr = tmem_base + lane_off + b * 128 + part * CW;
         ptx::mbar_wait(&tfull[b], (g >> 1) & 1);
         if (warp == kSattnSoft0 && lane == 0) SATTN_TR(4, g);
         __syncwarp();
         ptx::tc_fence_after();
-        float mt = -INFINITY;  // this half-tile's max: both 32-column loads in flight at once
+        float mt = -INFINITY;  // this part's max: its 32-column loads in flight at once
         {
-          uint32_t x[32], y[32];
-          ptx::tmem_ld_x32p(s_addr, x);
-          ptx::tmem_ld_x32p(s_addr + 32, y);
-          ptx::tmem_wait_ld_dep32p(x);
-          ptx::tmem_wait_ld_dep32p(y);
-          if (nv >= 64) {  // full half-tile (all but a row's last tile): no per-column masks
+          uint32_t x[CW / 32][32];
+#pragma unroll
+          for (int u = 0; u < CW / 32; ++u) ptx::tmem_ld_x32p(s_addr + 32 * u, x[u]);
+#pragma unroll
+          for (int u = 0; u < CW / 32; ++u) ptx::tmem_wait_ld_dep32p(x[u]);
+          if (nv >= CW) {  // a full part (all but a row's last tile): no per-column masks
             float m2[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int c = 0; c < 32; ++c) m2[c & 3] = fmaxf(m2[c & 3], fmaxf(__uint_as_float(x[c]), __uint_as_float(y[c])));
+            for (int u = 0; u < CW / 32; ++u)
+#pragma unroll
+              for (int c = 0; c < 32; ++c) m2[c & 3] = fmaxf(m2[c & 3], __uint_as_float(x[u][c]));
             mt = fmaxf(fmaxf(m2[0], m2[1]), fmaxf(m2[2], m2[3]));
           } else {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              if (c < nv) mt = fmaxf(mt, __uint_as_float(x[c]));
-              if (32 + c < nv) mt = fmaxf(mt, __uint_as_float(y[c]));
-            }
+            for (int u = 0; u < CW / 32; ++u)
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (32 * u + c < nv) mt = fmaxf(mt, __uint_as_float(x[u][c]));
           }
         }
-        sMax[b][half][head] = mt;
-        ptx::named_bar_sync(1, 256);
-        mt = fmaxf(sMax[b][0][head], sMax[b][1][head]) * sl;  // scale > 0
+        sMax[b][part][head] = mt;
+        ptx::named_bar_sync(1, kSattnSoftThreads);
+#pragma unroll
+        for (int u = 0; u < kSattnSplit; ++u) mt = fmaxf(mt, sMax[b][u][head]);
+        mt *= sl;  // scale > 0
         if (warp == kSattnSoft0 && lane == 0) SATTN_TR(5, g);
         // P of the previous tile consumed: O is stable and sP free
         ptx::mbar_wait(pempty, (g & 1) ^ 1);
         if (warp == kSattnSoft0 && lane == 0) SATTN_TR(7, g);
         __syncwarp();
-        if (mt > m + kLazy) {  // raise the max; rescale this half of O and l (not on the first tile)
+        if (mt > m + kLazy) {  // raise the max; rescale this part of O and l (not on the first tile)
           const float alpha = fast_exp2(m - mt);
           l2 = __fmul2_rn(l2, make_float2(alpha, alpha));
           if (j > 0) {
             ptx::tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < OH; c += 32) {
-              uint32_t o[32];
-              ptx::tmem_ld_x32p(o_addr + half * OH + c, o);
-              ptx::tmem_wait_ld_dep32p(o);
+            for (int c = 0; c < OP; c += OC) {
+              uint32_t o[OC];
+              ld_o(o_addr + c, o);
 #pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st_x32(o_addr + half * OH + c, o);
+              for (int e = 0; e < OC; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              if constexpr (OC == 32) tmem_st_x32(o_addr + c, o);
+              else tmem_st_x16(o_addr + c, o);
             }
             tmem_wait_st();
           }
           m = mt;
         }
-        // P (this head, this half's 64 tokens = one SW128 atom) in bf16 from a second read of S:
-        // packed f32x2 scale-and-shift and sum; l sums the unrounded P (as flash attention does)
+        // P (this head, this part's tokens) in bf16 from a second read of S: packed f32x2
+        // scale-and-shift and sum; l sums the unrounded P (as flash attention does)
         {
           const float2 nm2 = make_float2(-m, -m);
           float2 lb2 = make_float2(0.f, 0.f);  // a second accumulator: two shorter FADD2 chains
 #pragma unroll
-          for (int c0 = 0; c0 < 64; c0 += 32) {
+          for (int c0 = 0; c0 < CW; c0 += 32) {
             uint32_t x[32];
             ptx::tmem_ld_x32p(s_addr + c0, x);
             ptx::tmem_wait_ld_dep32p(x);
@@ -466,7 +498,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
                 const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                 pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
               }
-              *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, half * 64 + c0 + c, C::ATOM)) =
+              *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, part * CW + c0 + c, C::ATOM)) =
                   make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
           }
@@ -480,52 +512,60 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
         ptx::mbar_arrive(pfull);
         if (warp == kSattnSoft0 && lane == 0) SATTN_TR(8, g);
       }
-      // epilogue: O row / l of this head (this half of its DV columns) -> out[t][head]
-      sL[half][head] = l2.x + l2.y;
-      ptx::named_bar_sync(1, 256);
-      const float lt = sL[0][head] + sL[1][head];
+      // epilogue: O row / l of this head (this part of its DV columns) -> out[t][head]
+      sL[part][head] = l2.x + l2.y;
+      ptx::named_bar_sync(1, kSattnSoftThreads);
+      float lt = 0.f;
+#pragma unroll
+      for (int u = 0; u < kSattnSplit; ++u) lt += sL[u][head];
       const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
       ptx::mbar_wait(ofull, rr & 1);
       if (warp == kSattnSoft0 && lane == 0) SATTN_TR(11, rr);
       __syncwarp();
       ptx::tc_fence_after();
-      // O / l through this warp's 4 KB of sP (free: the row's PVs are complete) — 32 heads x 32
-      // columns, 16-byte chunks XOR-swizzled by row — so each global store writes four whole
-      // 128-byte row segments instead of 32 scattered 16-byte pieces
-      uint8_t* stg = sP + (warp - kSattnSoft0) * 4096;
-      const uint32_t stg_a = ptx::smem_u32(stg);
+      // O / l through this warp's share of sP (free: the row's PVs are complete) — 32 heads x
+      // EC columns, 16-byte chunks XOR-swizzled by row — so each global store writes whole
+      // row segments (4 x 128 B or 8 x 64 B) instead of 32 scattered 16-byte pieces
+      constexpr int NC = EC / 4;                                       // 16-byte chunks per row
+      constexpr int RPI = 32 / NC;                                     // rows per warp instruction
+      static_assert(OP % EC == 0 && EC % OC == 0, "epilogue staging tiles O's columns");
+      const uint32_t stg_a = ptx::smem_u32(sP + (warp - kSattnSoft0) * (C::P_BYTES / (4 * kSattnSplit)));
+      auto swz = [](int r, int c4) { return (r * NC + (c4 ^ ((r / (8 / NC)) & (NC - 1)))) * 16; };
+      const float f = n > 0 ? inv_l : 0.f;  // a row without tokens: O was never written, its output is 0
 #pragma unroll
-      for (int c = 0; c < OH; c += 32) {
-        uint32_t o[32];
-        ptx::tmem_ld_x32p(o_addr + half * OH + c, o);
-        ptx::tmem_wait_ld_dep32p(o);
-        const float f = n > 0 ? inv_l : 0.f;  // a row without tokens: O was never written, its output is 0
+      for (int c = 0; c < OP; c += EC) {
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 v = make_float4(__uint_as_float(o[4 * c4]) * f, __uint_as_float(o[4 * c4 + 1]) * f,
-                                       __uint_as_float(o[4 * c4 + 2]) * f, __uint_as_float(o[4 * c4 + 3]) * f);
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg_a + (lane * 8 + (c4 ^ (lane & 7))) * 16),
-                       "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                       : "memory");
+        for (int cc = 0; cc < EC; cc += OC) {
+          uint32_t o[OC];
+          ld_o(o_addr + c + cc, o);
+#pragma unroll
+          for (int q4 = 0; q4 < OC / 4; ++q4) {
+            const int c4 = cc / 4 + q4;
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg_a + swz(lane, c4)),
+                         "f"(__uint_as_float(o[4 * q4]) * f), "f"(__uint_as_float(o[4 * q4 + 1]) * f),
+                         "f"(__uint_as_float(o[4 * q4 + 2]) * f), "f"(__uint_as_float(o[4 * q4 + 3]) * f)
+                         : "memory");
+          }
         }
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = i * 4 + (lane >> 3), c4 = lane & 7;
+        for (int i = 0; i < 32 / RPI; ++i) {
+          const int r = i * RPI + lane / NC, c4 = lane % NC;
           float4 v;
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                       : "r"(stg_a + (r * 8 + (c4 ^ (r & 7))) * 16)
+                       : "r"(stg_a + swz(r, c4))
                        : "memory");
           const int hr = quad * 32 + r;
-          if (hr < a.H) *reinterpret_cast<float4*>(a.out + ((int64_t)t * a.H + hr) * DV + half * OH + c + c4 * 4) = v;
+          if (hr < a.H)
+            *reinterpret_cast<float4*>(a.out + ((int64_t)t * a.H + hr) * DV + part * OP + c + c4 * 4) = v;
         }
-        __syncwarp();  // the staging tile is rewritten by the next chunk
+        __syncwarp();  // the staging tile is rewritten by the next pass
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(oempty);
       if (warp == kSattnSoft0 && lane == 0) SATTN_TR(12, rr);
-      ptx::named_bar_sync(1, 256);  // sL is rewritten by the next row
+      ptx::named_bar_sync(1, kSattnSoftThreads);  // sL is rewritten by the next row
     }
   }
   ptx::tc_fence_before();
