@@ -132,6 +132,26 @@ def test_select_batch_host_pipeline_equals_device_path():
     assert not host.is_cuda and torch.equal(host, dev.cpu())
 
 
+def test_host_pipeline_ragged_prefixes_and_chunk_counts():
+    """The host pipeline (row chunks processed last rows first, the first chunk split again,
+    a ring of device buffers) returns the device path's top-k for arbitrary prefix lengths and
+    every chunk count, including more chunks than rows fit evenly."""
+    import numpy as np
+    import torch
+    from paper_2605_07363_b200 import IndexerEngine
+    g = torch.Generator().manual_seed(5)
+    L, T, H, d = 9000, 3001, 32, 128
+    K = torch.randn(L, d, generator=g).bfloat16()
+    Q = torch.randn(T, H, d, generator=g).bfloat16()
+    W = torch.softmax(torch.randn(T, H, generator=g), -1).float()
+    pl = np.random.default_rng(5).integers(1, L + 1, T)
+    eng = IndexerEngine("misa", budget_k=256, active_heads_h=4, block_size=256)
+    dev = eng.run(K.cuda(), Q.cuda(), W.cuda(), prefix_len=pl).topk.cpu()
+    for chunks in (1, 3, 8, 13):
+        host = eng.run_host(K.pin_memory(), Q.pin_memory(), W.pin_memory(), pl, chunks=chunks)
+        assert torch.equal(host, dev), chunks
+
+
 def test_constructive_needle_retrieval():
     """Acceptance criterion 5 (``test_acceptance.py:203-243``) through the GPU registry:
     margin-10, 32-token needles aligned with the top-gate head are fully retrieved by the
