@@ -42,6 +42,7 @@
  *   misa_relevance_dots   dsa.py:18-34       relevance_dots (raw per-query dot products)
  *   misa_pack_rows_f64    workload.py:202-254 load_workload payload (f64) -> device bf16 layouts
  *   misa_sparse_attention (no reference counterpart: PAPER.md Eq. 3, the selection's consumer)
+ *   misa_quant_rows_fp8   (no reference counterpart: FP8 upstream indexer projections)
  */
 #ifndef MISA_B200_H_
 #define MISA_B200_H_
@@ -299,6 +300,12 @@ int misa_list_prune(const float* scores, const int32_t* idx, int64_t ld, int64_t
  * blocks of `block` keys) -> global index ((i / block) * n_shards + shard) * block + i % block;
  * -1 entries are kept. */
 int misa_shard_map_indices(int32_t* idx, int64_t n, int block, int n_shards, int shard, void* stream);
+
+/* Row-wise FP8 e4m3 quantization (the upstream indexer projections' activations / weights):
+ * x (n_rows, cols) bf16 -> out (n_rows, cols) e4m3 bytes with scales[r] = amax_r / 448, so that
+ * x[r][c] ~= e4m3(out[r][c]) * scales[r] (round to nearest, saturating; a zero row gets scale 1).
+ * cols % 8 == 0; x 16-byte and out 8-byte aligned. */
+int misa_quant_rows_fp8(const void* x, int64_t n_rows, int cols, void* out, float* scales, void* stream);
 
 #ifdef __cplusplus
 }

@@ -22,13 +22,14 @@ from .dsa import dsa_rescore, dsa_score, dsa_select, gated_relu_scores, relevanc
 from .routing import misa_hier_select, misa_score, misa_select, route_head_importance, route_topk_heads
 from .corpus import Corpus, read_header, save_corpus, select_corpus
 from .sparse_attention import sparse_attention
+from .projections import IndexerProjections, quantize_rows_fp8
 from .estimators import (INDEXER_REGISTRY, METHODS, BaseTokenIndexer, DSAIndexer, HierarchicalMISAIndexer,
                          MISAIndexer, make_indexer)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "Corpus", "sparse_attention", "DecodeGraph", "PagedKeyCache", "PrecisionWarning", "read_header", "save_corpus", "select_corpus",
+    "Corpus", "sparse_attention", "IndexerProjections", "quantize_rows_fp8", "DecodeGraph", "PagedKeyCache", "PrecisionWarning", "read_header", "save_corpus", "select_corpus",
     "BASELINE_BLOCK_SIZE", "BLOCK_ATTENTION", "BaseTokenIndexer", "BlockSummary", "CostEntry", "CostLedger",
     "DSAIndexer", "FAST32", "GATE_ONLY", "HeadSet", "HierarchicalMISAIndexer", "INDEXER_REGISTRY", "IndexerConfig",
     "IndexerEngine", "IndexerOutput", "IndexerWorkload", "METHODS", "MISAIndexer", "NeedleLabel", "PRECISION_MODES",

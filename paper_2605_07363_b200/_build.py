@@ -21,7 +21,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libmisa_b200.so")
-SOURCES = ["abi.cu", "pool.cu", "router.cu", "score.cu", "select.cu", "refine.cu", "pack.cu", "sattn.cu"]
+SOURCES = ["abi.cu", "pool.cu", "router.cu", "score.cu", "select.cu", "refine.cu", "pack.cu", "sattn.cu", "quant.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", os.path.join(REPO, "include")]

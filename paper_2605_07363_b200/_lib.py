@@ -67,6 +67,7 @@ SIGNATURES: dict[str, list] = {
     "misa_sparse_attention": [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _i64, _i32, _i32, _f32, _vp, _vp],
     "misa_relevance_dots": [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _i64, _vp],
     "misa_pack_rows_f64": [_vp, _i64, _i32, _i64, _i64, _vp, _i32, _i64, _vp, _vp],
+    "misa_quant_rows_fp8": [_vp, _i64, _i32, _vp, _vp, _vp],
 }
 EXTRA = {"misa_abi_version": ([], ctypes.c_int), "misa_last_error": ([], ctypes.c_char_p),
          "misa_sm_count": ([], ctypes.c_int)}

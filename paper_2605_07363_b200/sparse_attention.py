@@ -7,7 +7,7 @@ together with the attention it feeds.
 
 with one latent row c[s] per token shared by all heads (MQA), T_t = the indexer's top-k of
 row t (ascending, -1 padded).  ``misa_sparse_attention`` (csrc/sattn.cu): tcgen05, the
-selected rows gathered 128 at a time, two-pass softmax, P in bf16.
+selected rows gathered 128 at a time, online softmax with a lazily raised max, P in bf16.
 """
 
 from __future__ import annotations
@@ -31,8 +31,11 @@ def sparse_attention(queries: torch.Tensor, kv: torch.Tensor, topk: torch.Tensor
     if H > 128:
         raise ValueError("at most 128 query heads per row")
     dev = queries.device
-    q = torch.zeros(T, 128, d, dtype=torch.bfloat16, device=dev)
-    q[:, :H] = queries.to(torch.bfloat16)
+    if H == 128 and queries.dtype == torch.bfloat16 and queries.is_contiguous():
+        q = queries  # already the kernel's layout: no padded copy
+    else:
+        q = torch.zeros(T, 128, d, dtype=torch.bfloat16, device=dev)
+        q[:, :H] = queries.to(torch.bfloat16)
     c = kv.to(torch.bfloat16).contiguous()
     tk = topk.to(torch.int32)
     if tk.stride(1) != 1:
