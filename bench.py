@@ -535,6 +535,25 @@ def run_ours(a):
         del qa
         torch.cuda.empty_cache()
 
+    # --- the indexer's producer: FP8 upstream projections of this layer's rows
+    proj = None
+    if world == 1 and not a.no_sattn:
+        from paper_2605_07363_b200 import IndexerProjections
+        dm, dqc = 7168, 1536  # DeepSeek-V3.2: hidden size, query latent
+        pj = IndexerProjections(dm, a.H, a.d, d_q=dqc, seed=2)
+        gh = torch.Generator(device="cuda").manual_seed(3)
+        hid = torch.randn(T, dm, device="cuda", generator=gh).bfloat16()
+        cql = torch.randn(T, dqc, device="cuda", generator=gh).bfloat16()
+        ms_pj = _time_steps(lambda: pj(hid, cql), 3, 1, barrier)
+        fl = 2.0 * T * (dqc * a.H * a.d + dm * (a.d + a.H))
+        proj = {"workload": f"FP8 e4m3 projections of T={T} rows: q from a {dqc}-wide query latent "
+                            f"({a.H}x{a.d}), k and signed w from {dm}-wide hidden states; per-token "
+                            f"activation quantization included",
+                "ms": round(ms_pj, 3), "TFLOP_s": round(fl / ms_pj / 1e9, 1),
+                "note": "cuBLASLt row-wise-scaled FP8 GEMMs (library) + misa_quant_rows_fp8"}
+        del hid, cql, pj
+        torch.cuda.empty_cache()
+
     c5 = None
     if world == 1 and not a.no_c5:
         del eng_m, eng_d, x
@@ -564,7 +583,7 @@ def run_ours(a):
         "fallback_rows": fallback,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         "decode": decode, "sharded_decode": sdec, "configs": sweep, "c5_prefill": c5, "needle": needle,
-        "sparse_attention": sattn,
+        "sparse_attention": sattn, "fp8_projections": proj,
     }
     if hier_ms is not None:
         line["misa_hier_ms_per_layer"] = round(hier_ms, 3)
