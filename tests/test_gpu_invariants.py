@@ -1,6 +1,8 @@
 """The reference's invariants (pkg/tests/test_routing.py, test_dsa.py) on the device path, plus a
 hypothesis sweep of small random workloads against the oracle."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -81,7 +83,9 @@ def test_dense_selection_head_permutation_invariance():
     assert _near_tie_ok(a, b, scores, mag, 300)
 
 
-@settings(max_examples=30, deadline=None, derandomize=True)
+# MISA_HYPOTHESIS_EXAMPLES / MISA_HYPOTHESIS_SEED widen the sweep (default: 30 fixed examples)
+@settings(max_examples=int(os.environ.get("MISA_HYPOTHESIS_EXAMPLES", 30)), deadline=None,
+          derandomize="MISA_HYPOTHESIS_SEED" not in os.environ)
 @given(L=st.integers(1, 700), H=st.sampled_from([4, 8, 16]), d=st.sampled_from([16, 32, 64]),
        k=st.integers(1, 260), h=st.integers(1, 8), B=st.sampled_from([1, 7, 64, 128]),
        raw=st.booleans(), seed=st.integers(0, 10_000))
