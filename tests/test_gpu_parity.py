@@ -372,3 +372,49 @@ def test_prefill_selector_equals_decode_selector(method, H, h, d, B, k):
     assert torch.equal(dec.topk, pre.topk[rows]), method
     if method != "dsa":
         assert torch.equal(dec.heads, pre.heads[rows])
+
+
+hypothesis = pytest.importorskip("hypothesis")
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=int(os.environ.get("MISA_HYPOTHESIS_EXAMPLES_MEDIUM", 8)), deadline=None,
+          derandomize="MISA_HYPOTHESIS_SEED" not in os.environ)
+@given(L=st.integers(3000, 24000), H=st.sampled_from([16, 32, 64]), h=st.sampled_from([2, 4, 8]),
+       B=st.sampled_from([64, 128, 256, 1024]), k=st.sampled_from([32, 100, 512, 1000]),
+       signed=st.booleans(), ragged=st.booleans(), seed=st.integers(0, 10_000))
+def test_random_medium_workloads_fused_path(L, H, h, B, k, signed, ragged, seed):
+    """Random medium workloads where the fused τ-filter and the persistent selector run (rows
+    well past k): causal or ragged prefix lengths, signed or softmax gates; DSA and MISA rows
+    (incl. the longest) against the oracle with the tie census."""
+    from paper_2605_07363_b200 import IndexerEngine
+    rng = np.random.default_rng(seed)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    T = L if not ragged else int(rng.integers(200, 2000))
+    K = torch.randn(L, 128, device="cuda", generator=gen).bfloat16()
+    Q = torch.randn(T, H, 128, device="cuda", generator=gen).bfloat16()
+    g = torch.randn(T, H, device="cuda", generator=gen)
+    W = (g * 0.5 if signed else torch.softmax(g, -1)).float()
+    pl = rng.integers(1, L + 1, T) if ragged else None
+    n_of = (lambda t: int(pl[t])) if ragged else (lambda t: t + 1)
+    eng_d = IndexerEngine("dsa", budget_k=k)
+    eng_m = IndexerEngine("misa", budget_k=k, active_heads_h=h, block_size=B)
+    r_d = eng_d.run(K, Q, W, pl)
+    r_m = eng_m.run(K, Q, W, pl, need_importance=True)
+    torch.cuda.synchronize()
+    longest = int(np.argmax(pl)) if ragged else T - 1
+    rows = sorted(set([longest] + rng.integers(0, T, 3).tolist()))
+    Kn = K.double().cpu().numpy()
+    cd, cm = Census(), Census()
+    for t in rows:
+        n = n_of(t)
+        qs, ws = Q[t].double().cpu().numpy(), W[t].double().cpu().numpy()
+        check_topk(r_d.topk[t].cpu().numpy(), O.gated_relu_scores(Kn[:n], qs, ws, "fast32"), _mag(Kn[:n], qs, ws),
+                   k, cd, f"dsa t={t}")
+        _, pooled = O.block_pool(Kn[:n], B)
+        E = O.route_head_importance(qs, ws, pooled, precision="fast32")
+        gh = r_m.heads[t].cpu().numpy()
+        check_heads(gh, E, min(h, H), f"heads t={t}")
+        gh = gh[gh >= 0]
+        hm = np.abs(ws[gh]) @ np.abs(qs[gh] @ Kn[:n].T)
+        check_topk(r_m.topk[t].cpu().numpy(), O.misa_score(Kn[:n], qs, ws, gh, "fast32"), hm, k, cm, f"misa t={t}")
