@@ -418,3 +418,50 @@ def test_random_medium_workloads_fused_path(L, H, h, B, k, signed, ragged, seed)
         gh = gh[gh >= 0]
         hm = np.abs(ws[gh]) @ np.abs(qs[gh] @ Kn[:n].T)
         check_topk(r_m.topk[t].cpu().numpy(), O.misa_score(Kn[:n], qs, ws, gh, "fast32"), hm, k, cm, f"misa t={t}")
+
+
+@settings(max_examples=int(os.environ.get("MISA_HYPOTHESIS_EXAMPLES_MEDIUM", 6)), deadline=None,
+          derandomize="MISA_HYPOTHESIS_SEED" not in os.environ)
+@given(L=st.integers(3000, 20000), H=st.sampled_from([32, 64]), h=st.sampled_from([4, 8]),
+       B=st.sampled_from([128, 1024]), k=st.sampled_from([64, 256, 512]), mult=st.sampled_from([2, 4]),
+       ragged=st.booleans(), seed=st.integers(0, 10_000))
+def test_random_medium_misa_hier(L, H, h, B, k, mult, ragged, seed):
+    """MISA-dagger on random medium workloads: the coarse routed top-k' (fused filter + runs
+    selector) and the all-head re-rank inside it (routing.py:144-174), against the oracle."""
+    from paper_2605_07363_b200 import IndexerEngine
+    rng = np.random.default_rng(seed)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    kp = mult * k
+    T = L if not ragged else int(rng.integers(200, 1500))
+    K = torch.randn(L, 128, device="cuda", generator=gen).bfloat16()
+    Q = torch.randn(T, H, 128, device="cuda", generator=gen).bfloat16()
+    W = torch.softmax(torch.randn(T, H, device="cuda", generator=gen), -1).float()
+    pl = rng.integers(1, L + 1, T) if ragged else None
+    eng = IndexerEngine("misa_hier", budget_k=k, active_heads_h=h, block_size=B, candidate_kprime=kp)
+    r = eng.run(K, Q, W, pl)
+    torch.cuda.synchronize()
+    cand_all = r.sorted_candidates().cpu().numpy()
+    longest = int(np.argmax(pl)) if ragged else T - 1
+    Kn = K.double().cpu().numpy()
+    cc, cf = Census(), Census()
+    for t in sorted(set([longest] + rng.integers(0, T, 2).tolist())):
+        n = int(pl[t]) if ragged else t + 1
+        keys, qs, ws = Kn[:n], Q[t].double().cpu().numpy(), W[t].double().cpu().numpy()
+        gh = r.heads[t].cpu().numpy()
+        gh = gh[gh >= 0]
+        ms = O.misa_score(keys, qs, ws, gh, "fast32")
+        hm = np.abs(ws[gh]) @ np.abs(qs[gh] @ keys.T)
+        cand = cand_all[t]
+        check_topk(cand, ms, hm, kp, cc, f"hier-coarse t={t}")
+        cand = cand[cand >= 0]
+        fine = O.gated_relu_scores(keys[cand], qs, ws, "fast32")
+        exp = O.topk_within(fine, cand, k)
+        got = r.topk[t].cpu().numpy()
+        got = got[got >= 0]
+        assert got.shape[0] == min(k, n)
+        if got.tolist() != exp.tolist():
+            kth = np.sort(fine)[::-1][min(k, cand.shape[0]) - 1]
+            fm = _mag(keys[cand], qs, ws)
+            pos = {c: j for j, c in enumerate(cand.tolist())}
+            for c in set(got.tolist()) ^ set(exp.tolist()):
+                assert abs(fine[pos[c]] - kth) <= TAU_S * (fm[pos[c]] + abs(kth)), (t, c)
