@@ -13,12 +13,18 @@
 // max: P = exp2(S - m) in bf16 to shared memory (the K-major A operand), O accumulated in
 // TMEM and rescaled in place only when a tile's max exceeds m by more than 2^8; O / l at the
 // end.  S is double-buffered in TMEM so the next tile's QK overlaps this tile's softmax.
-// A row's selected tokens come first, -1 padding after (the indexer's output): every role
-// finds the row's count n with a binary search and walks ceil(n / 128) tiles; slots past n
-// in the last tile are zero-filled and masked to probability 0; a row with no token gets 0.
+// A row's selected tokens come first, -1 padding after (the indexer's output): the Q loader
+// counts them (warp-collective, two dependent load rounds) and publishes n in a ring of smem
+// slots (one mbarrier each) for the MMA and softmax warps; the producers count for themselves
+// one row ahead; every role walks ceil(n / 128) tiles; slots past n in the last tile are
+// zero-filled and masked to probability 0; a row with no token gets 0.  The Q loader also
+// prefetches the next row's Q and selection into L2 and loads a row's Q as soon as the
+// previous row's last QK is done; the epilogue stages O / l through shared memory so its
+// global stores write whole row segments.
 //
-// Warps: 0-3 gather producers, 4 MMA issuer, 13 Q loader / L2 prefetcher, 5-12 softmax /
-// epilogue (thread = head and half of its columns, TMEM lane quadrant = warp % 4).
+// Warps: 0-3 gather producers, 4 MMA issuer, 5 .. 5 + 4 * kSattnSplit - 1 softmax / epilogue
+// (thread = head and 1/kSattnSplit of its columns, TMEM lane quadrant = warp % 4), then the
+// Q loader / L2 prefetcher (warp 13 for the default split of 2).
 #include "common.cuh"
 #include "ptx.cuh"
 
