@@ -156,6 +156,10 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 // rare after the first tiles.
 constexpr float kLazy = 8.f;
 
+#ifndef MISA_SATTN_PTMEM
+#define MISA_SATTN_PTMEM 1  // P through TMEM (A operand of P V read from TMEM) when the columns fit
+#endif
+
 #ifdef MISA_SATTN_TRACE
 // dev instrumentation (tools/sattn_trace.py): clock64 stamps of CTA 0's pipeline events
 constexpr int kTrEv = 16, kTrN = 1024;
@@ -174,6 +178,11 @@ template <int DQK, int DV>
 __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_constant__ CUtensorMap tmap_q, const SattnArgs a) {
   using C = SattnCfg<DQK>;
   constexpr int STAGES = C::STAGES;
+  // P in TMEM after S0 | S1 | O (DV columns) when 64 more columns fit: the softmax writes it
+  // with one tcgen05.st per 32 tokens and P V reads it as a TMEM A operand (no smem round
+  // trip, no async-proxy fence); otherwise P goes through shared memory (K-major SW128)
+  constexpr bool PT = MISA_SATTN_PTMEM && 256 + DV + 64 <= 512;
+  constexpr uint32_t kPCol = 256 + DV;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = ptx::align_smem_1024(smem_raw);
   uint8_t* sQ = smem + C::OFF_Q;
@@ -366,8 +375,12 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
 #pragma unroll
           for (int kk = 0; kk < 128 / 16; ++kk) {  // K = this tile's 128 tokens
             const uint32_t koff = (kk & 3) * 32;
-            ptx::mma_bf16(o_tmem, ptx::sw128_kmajor_desc(p_base + (kk >> 2) * C::ATOM + koff),
-                          sw128_mnmajor_desc(kv_base + kk * 2048, kLbo, kSbo), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+            if constexpr (PT)
+              ptx::mma_bf16_ts(o_tmem, tmem_base + kPCol + kk * 8, sw128_mnmajor_desc(kv_base + kk * 2048, kLbo, kSbo),
+                               idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+            else
+              ptx::mma_bf16(o_tmem, ptx::sw128_kmajor_desc(p_base + (kk >> 2) * C::ATOM + koff),
+                            sw128_mnmajor_desc(kv_base + kk * 2048, kLbo, kSbo), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[s]);
           ptx::mma_commit(pempty);
@@ -481,6 +494,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
             ptx::tmem_ld_x32p(s_addr + c0, x);
             ptx::tmem_wait_ld_dep32p(x);
             const bool full_chunk = nv >= c0 + 32;
+            uint32_t pk16[16];  // PT: this chunk's 32 probabilities, two bf16 per TMEM column
 #pragma unroll
             for (int c = 0; c < 32; c += 8) {
               uint32_t pk[4];
@@ -504,16 +518,23 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
                 const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                 pk[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
               }
-              *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, part * CW + c0 + c, C::ATOM)) =
-                  make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              if constexpr (PT) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) pk16[c / 2 + u] = pk[u];
+              } else {
+                *reinterpret_cast<uint4*>(sP + ptx::sw128_offset(head, part * CW + c0 + c, C::ATOM)) =
+                    make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              }
             }
+            if constexpr (PT) tmem_st_x16(tmem_base + lane_off + kPCol + (part * CW + c0) / 2, pk16);
           }
           l2 = __fadd2_rn(l2, lb2);
+          if constexpr (PT) tmem_wait_st();
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[b]);  // S read twice (max, then P): the buffer can be refilled
         if (warp == kSattnSoft0 && lane == 0) SATTN_TR(6, g);
-        ptx::fence_proxy_async_smem();  // generic P writes -> the PV MMA's operand reads
+        if constexpr (!PT) ptx::fence_proxy_async_smem();  // generic P writes -> the PV MMA's operand reads
         ptx::tc_fence_before();         // the O rescale (tcgen05.st) before the next MMA
         ptx::mbar_arrive(pfull);
         if (warp == kSattnSoft0 && lane == 0) SATTN_TR(8, g);
