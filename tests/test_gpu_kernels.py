@@ -151,7 +151,7 @@ def test_router_matches_fp32(H, D, B, L, h):
     n_chunks = max(1, (nf + 127) // 128)
     rows = n_chunks * 128
     P = torch.empty(L, D, device="cuda")
-    planes = torch.empty(3, rows, D, device="cuda").bfloat16()
+    planes = torch.empty(3, rows, D, device="cuda", dtype=torch.bfloat16)  # written by the kernel
     lib = _lib()
     lib.call("misa_pool_keys", _p(K), L, D, B, _p(P), None, _p(planes), rows, _stream())
     it_tile, it_chunk, it_cols, n_items = _route_items(prefix.cpu(), T, H, B, n_chunks)

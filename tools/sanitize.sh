@@ -7,7 +7,7 @@ set -u
 TAG=${1:-r02}
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
-TESTS="tests/test_gpu_kernels.py tests/test_gpu_varlen.py tests/test_gpu_decode.py tests/test_gpu_boundary.py tests/test_gpu_invariants.py tests/test_gpu_sparse_attention.py"
+TESTS="tests/test_gpu_kernels.py tests/test_gpu_varlen.py tests/test_gpu_decode.py tests/test_gpu_boundary.py tests/test_gpu_invariants.py tests/test_gpu_sparse_attention.py tests/test_gpu_projections.py"
 SEL="not c4 and not c5 and not 1048576"
 for tool in memcheck racecheck synccheck initcheck; do
   log=gpurun_out/${TAG}_sanitize_${tool}.log
