@@ -156,6 +156,9 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 // rare after the first tiles.
 constexpr float kLazy = 8.f;
 
+#ifndef MISA_SATTN_QBAR
+#define MISA_SATTN_QBAR 1  // per-quadrant named barriers for the softmax exchanges
+#endif
 #ifndef MISA_SATTN_PTMEM
 #define MISA_SATTN_PTMEM 1  // P through TMEM (A operand of P V read from TMEM) when the columns fit
 #endif
@@ -402,6 +405,13 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
     constexpr int OC = OP < EC ? OP : EC;  // O columns per TMEM load / store (16 or 32)
     const int quad = warp & 3;
     const int part = (warp - kSattnSoft0) >> 2;
+    // the max / sum exchanges are per head: only the kSattnSplit warps of one lane quadrant
+    // meet (one named barrier per quadrant), so quadrants never wait for each other
+#if MISA_SATTN_QBAR
+    const uint32_t kQBarId = 1 + quad, kQBarThreads = 32 * kSattnSplit;
+#else
+    const uint32_t kQBarId = 1, kQBarThreads = kSattnSoftThreads;
+#endif
     const int head = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t o_addr = tmem_base + lane_off + 256 + part * OP;
@@ -456,7 +466,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
           }
         }
         sMax[b][part][head] = mt;
-        ptx::named_bar_sync(1, kSattnSoftThreads);
+        ptx::named_bar_sync(kQBarId, kQBarThreads);
 #pragma unroll
         for (int u = 0; u < kSattnSplit; ++u) mt = fmaxf(mt, sMax[b][u][head]);
         mt *= sl;  // scale > 0
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
       }
       // epilogue: O row / l of this head (this part of its DV columns) -> out[t][head]
       sL[part][head] = l2.x + l2.y;
-      ptx::named_bar_sync(1, kSattnSoftThreads);
+      ptx::named_bar_sync(kQBarId, kQBarThreads);
       float lt = 0.f;
 #pragma unroll
       for (int u = 0; u < kSattnSplit; ++u) lt += sL[u][head];
@@ -592,7 +602,7 @@ __global__ void __launch_bounds__(kSattnThreads, 1) sattn_kernel(const __grid_co
       ptx::tc_fence_before();
       ptx::mbar_arrive(oempty);
       if (warp == kSattnSoft0 && lane == 0) SATTN_TR(12, rr);
-      ptx::named_bar_sync(1, kSattnSoftThreads);  // sL is rewritten by the next row
+      ptx::named_bar_sync(kQBarId, kQBarThreads);  // sL is rewritten by the next row
     }
   }
   ptx::tc_fence_before();
